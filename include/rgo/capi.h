@@ -1,0 +1,113 @@
+/*
+ * rgo/capi.h -- the C-ABI boundary of the B200 dropout-RNG pipeline.
+ *
+ * The reference (proj/include/rgo/*.hpp) is a header-only C++ library whose
+ * entry points are the plugin surface for this path.  Each function below is
+ * the device-side replacement for one of them; the C++ headers next to this
+ * file (include/rgo/philox.hpp, mask.hpp, ref_attention.hpp, workload.hpp)
+ * keep the reference's names and signatures and call through here.
+ *
+ * Conventions
+ *   - plain pointers + byte/element counts; no torch or C++ types;
+ *   - device pointers are prefixed d_, host pointers h_;
+ *   - rgo_stream_t is a cudaStream_t (NULL = legacy default stream); every
+ *     device call is stream-ordered and asynchronous;
+ *   - the library never allocates memory that it returns to the caller;
+ *   - every call returns an rgo_status; on failure rgo_last_error() returns a
+ *     thread-local message (validation messages keep the reference's keywords,
+ *     e.g. "bytes"/"guard" for the capacity guard, mask.hpp:148-155);
+ *   - there is no CPU fallback: with no CUDA device every compute call fails
+ *     with RGO_ENODEV.
+ */
+#ifndef RGO_CAPI_H
+#define RGO_CAPI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* rgo_stream_t; /* cudaStream_t */
+
+typedef enum rgo_status {
+    RGO_OK = 0,
+    RGO_EINVAL = 1,  /* std::invalid_argument in the reference */
+    RGO_ECUDA = 2,   /* CUDA runtime / launch failure */
+    RGO_ENOMEM = 3,  /* device allocation failed (host wrappers only) */
+    RGO_EIO = 4,     /* std::runtime_error in the reference (mask file I/O) */
+    RGO_ENODEV = 5   /* no CUDA device: the product has no CPU fallback */
+} rgo_status;
+
+const char* rgo_last_error(void);
+int rgo_version(void);
+/* Number of CUDA devices visible (0 on a CPU-only host). */
+int rgo_device_count(void);
+
+/* ---------------------------------------------------------------- philox --
+ * philox_block(key, counter, rounds) for n independent inputs on device
+ * (replaces proj/include/rgo/philox.hpp:84-96).  d_keys: n x {k0,k1},
+ * d_ctrs: n x {c0..c3}, d_rounds: n ints in [1,16] (unchecked on device),
+ * d_out: n x {w0..w3}. */
+int rgo_philox_blocks(const uint32_t* d_keys, const uint32_t* d_ctrs, const int32_t* d_rounds,
+                      uint32_t* d_out, uint64_t n, rgo_stream_t stream);
+
+/* ------------------------------------------------------------------ mask --
+ * Dropout mask layout (mask.hpp:24-48) + threshold + rounds. */
+typedef struct rgo_mask_desc {
+    uint32_t batch;
+    uint32_t heads;
+    uint32_t seq;          /* rows == cols == seq */
+    uint32_t rounds;       /* Philox rounds, [1,16] */
+    uint64_t seed;         /* key = (seed lo, seed hi), mask.hpp:41-43 */
+    uint64_t base_offset;  /* counter of block 0, mask.hpp:28 */
+    uint64_t threshold;    /* KeepThreshold::threshold(), [0, 2^32], mask.hpp:62-65 */
+} rgo_mask_desc;
+
+/* Launch shaping for the mask kernel (0 = automatic).  grid caps the
+ * persistent grid, dyn_smem reserves shared memory per CTA so the kernel only
+ * occupies the slots a concurrently running GEMM leaves free. */
+typedef struct rgo_launch {
+    uint32_t grid;
+    uint32_t block;
+    uint32_t dyn_smem;
+    uint32_t reserved;
+} rgo_launch;
+
+/* KeepThreshold(p) (mask.hpp:53-68): keep_prob rounded to float, threshold =
+ * llround(double(float p) * 2^32).  RGO_EINVAL unless 0 <= p <= 1. */
+int rgo_keep_threshold(double p, uint64_t* threshold, float* keep_prob);
+
+/* ceil(B*nH*SQ^2 / 8); RGO_EINVAL for an empty layout (mask.hpp:45-47). */
+int rgo_mask_bytes(const rgo_mask_desc* d, uint64_t* bytes);
+
+/* K1: write the packed keep mask of layout d into d_bits (bytes >=
+ * rgo_mask_bytes, 16-byte aligned).  Bit-exact with generate_mask
+ * (mask.hpp:142-179) for any layout, threshold and rounds. */
+int rgo_mask_generate(const rgo_mask_desc* d, uint8_t* d_bits, uint64_t bytes,
+                      rgo_stream_t stream);
+int rgo_mask_generate_ex(const rgo_mask_desc* d, uint8_t* d_bits, uint64_t bytes,
+                         const rgo_launch* launch, rgo_stream_t stream);
+
+/* Drop-in for generate_mask(layout, thr, rounds, workers): validates like the
+ * reference (rounds, empty layout, 2^36-bit guard with a message containing
+ * "bytes" and "guard"), generates on `devices` GPUs (0 = all visible; the
+ * reference's worker count maps to the device count -- output bytes do not
+ * depend on it, mask.hpp:139-141) and copies the bits to h_bits. */
+int rgo_generate_mask_host(const rgo_mask_desc* d, uint8_t* h_bits, uint64_t bytes,
+                           uint32_t devices);
+
+/* ------------------------------------------------------- synthetic inputs --
+ * random_attention_input's generator (ref_attention.hpp:186-202) on device:
+ * n values uniform in [-1,1) from Philox-10 with counter
+ * (i/4 lo, i/4 hi, stream_id, 0x5eed).  Writes fp32 (d_f32, exact) and/or
+ * bf16 (d_bf16, round-to-nearest of the fp32 value); either may be NULL. */
+int rgo_uniform_fill(uint64_t seed, uint32_t stream_id, uint64_t n, void* d_bf16, float* d_f32,
+                     rgo_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RGO_CAPI_H */

@@ -1,0 +1,18 @@
+"""paper_2410_07531_b200 -- B200-native dropout-RNG pipeline (arXiv 2410.07531).
+
+Python mirror of the reference's rgo:: API (proj/include/rgo/*.hpp) on top of
+the C-ABI library librgo_b200.so (hand-written sm_100a kernels).  See
+DESIGN.md for the path, boundary and kernels.
+"""
+from . import _lib
+from .philox import (PhiloxBlock, PhiloxCounter, PhiloxKey, advance, bump_key, philox_block,
+                     philox_blocks, philox_round)
+from .mask import (DropoutMask, KeepThreshold, MaskLayout, element_source, generate_mask,
+                   generate_mask_device, keep_bit_direct, load_mask, mask_bit, save_mask)
+
+__all__ = [
+    "PhiloxBlock", "PhiloxCounter", "PhiloxKey", "advance", "bump_key", "philox_block",
+    "philox_blocks", "philox_round", "DropoutMask", "KeepThreshold", "MaskLayout",
+    "element_source", "generate_mask", "generate_mask_device", "keep_bit_direct", "load_mask",
+    "mask_bit", "save_mask",
+]

@@ -1,0 +1,107 @@
+"""ctypes binding of the C-ABI boundary (include/rgo/capi.h).
+
+The shared library is built in-tree (paper_2410_07531_b200/librgo_b200.so,
+see csrc/Makefile).  Loading fails loudly when it is missing: there is no
+CPU fallback anywhere in the product path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librgo_b200.so")
+
+RGO_OK, RGO_EINVAL, RGO_ECUDA, RGO_ENOMEM, RGO_EIO, RGO_ENODEV = range(6)
+
+
+class RgoError(RuntimeError):
+    """Non-validation failure (CUDA, device, allocation)."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(msg)
+        self.code = code
+
+
+class RgoIOError(RgoError):
+    """Mirror of the reference's std::runtime_error for mask file I/O."""
+
+
+class mask_desc(C.Structure):
+    _fields_ = [
+        ("batch", C.c_uint32),
+        ("heads", C.c_uint32),
+        ("seq", C.c_uint32),
+        ("rounds", C.c_uint32),
+        ("seed", C.c_uint64),
+        ("base_offset", C.c_uint64),
+        ("threshold", C.c_uint64),
+    ]
+
+
+class launch(C.Structure):
+    _fields_ = [
+        ("grid", C.c_uint32),
+        ("block", C.c_uint32),
+        ("dyn_smem", C.c_uint32),
+        ("reserved", C.c_uint32),
+    ]
+
+
+# name -> (restype, argtypes).  Every symbol include/rgo/capi.h declares.
+SIGNATURES = {
+    "rgo_last_error": (C.c_char_p, []),
+    "rgo_version": (C.c_int, []),
+    "rgo_device_count": (C.c_int, []),
+    "rgo_philox_blocks": (
+        C.c_int,
+        [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p],
+    ),
+    "rgo_keep_threshold": (C.c_int, [C.c_double, C.POINTER(C.c_uint64), C.POINTER(C.c_float)]),
+    "rgo_mask_bytes": (C.c_int, [C.POINTER(mask_desc), C.POINTER(C.c_uint64)]),
+    "rgo_mask_generate": (C.c_int, [C.POINTER(mask_desc), C.c_void_p, C.c_uint64, C.c_void_p]),
+    "rgo_mask_generate_ex": (
+        C.c_int,
+        [C.POINTER(mask_desc), C.c_void_p, C.c_uint64, C.POINTER(launch), C.c_void_p],
+    ),
+    "rgo_generate_mask_host": (
+        C.c_int,
+        [C.POINTER(mask_desc), C.c_void_p, C.c_uint64, C.c_uint32],
+    ),
+    "rgo_uniform_fill": (
+        C.c_int,
+        [C.c_uint64, C.c_uint32, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p],
+    ),
+}
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load (once) the product library; raise if it is not built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `make -C paper_2410_07531_b200/csrc` "
+                "(or __graft_entry__.build()); the rgo B200 path has no CPU fallback"
+            )
+        dll = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(dll, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = dll
+    return _lib
+
+
+def check(code: int) -> None:
+    """Map an rgo_status to the reference's exception types."""
+    if code == RGO_OK:
+        return
+    msg = lib().rgo_last_error().decode(errors="replace")
+    if code == RGO_EINVAL:
+        raise ValueError(msg)  # std::invalid_argument
+    if code == RGO_EIO:
+        raise RgoIOError(code, msg)  # std::runtime_error
+    raise RgoError(code, msg)

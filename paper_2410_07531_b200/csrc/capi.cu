@@ -1,0 +1,217 @@
+// capi.cu -- implementation of the C-ABI boundary (include/rgo/capi.h):
+// argument validation with the reference's error semantics, error mapping,
+// and kernel launches.  No compute happens on the host; with no CUDA device
+// every compute entry point fails with RGO_ENODEV (there is no CPU fallback).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <algorithm>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "rgo/capi.h"
+#include "rgo_internal.h"
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+int fail(int code, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    std::vsnprintf(g_err, sizeof g_err, fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+    return fail(RGO_ECUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+int require_device() {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        return fail(RGO_ENODEV, "no CUDA device: the rgo B200 path has no CPU fallback");
+    }
+    return RGO_OK;
+}
+
+constexpr uint64_t kMaxBits = uint64_t{1} << 36;  // mask.hpp:108
+
+uint64_t elem_count(const rgo_mask_desc* d) {
+    return static_cast<uint64_t>(d->batch) * d->heads * d->seq * static_cast<uint64_t>(d->seq);
+}
+
+// MaskLayout::validate + rounds + threshold domain (mask.hpp:45-47, :145-146).
+int validate_mask(const rgo_mask_desc* d, const char* fn) {
+    if (!d) return fail(RGO_EINVAL, "%s: null descriptor", fn);
+    if (elem_count(d) == 0) return fail(RGO_EINVAL, "mask layout has zero elements");
+    if (d->rounds < 1 || d->rounds > 16)
+        return fail(RGO_EINVAL, "%s: rounds must be in [1,16]", fn);
+    if (d->threshold > (uint64_t{1} << 32))
+        return fail(RGO_EINVAL, "%s: threshold must be in [0, 2^32]", fn);
+    return RGO_OK;
+}
+
+}  // namespace
+
+namespace rgo {
+int num_sms() {
+    static int cached[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!cached[dev]) {
+        int n = 0;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        cached[dev] = n > 0 ? n : 148;
+    }
+    return cached[dev];
+}
+}  // namespace rgo
+
+extern "C" {
+
+const char* rgo_last_error(void) { return g_err; }
+
+int rgo_version(void) { return 1; }
+
+int rgo_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+int rgo_philox_blocks(const uint32_t* d_keys, const uint32_t* d_ctrs, const int32_t* d_rounds,
+                      uint32_t* d_out, uint64_t n, rgo_stream_t stream) {
+    if (int e = require_device()) return e;
+    if (n && (!d_keys || !d_ctrs || !d_rounds || !d_out))
+        return fail(RGO_EINVAL, "rgo_philox_blocks: null pointer");
+    cudaError_t e = rgo::launch_philox_blocks(d_keys, d_ctrs, d_rounds, d_out, n,
+                                              static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? RGO_OK : cuda_fail(e, "rgo_philox_blocks");
+}
+
+int rgo_keep_threshold(double p, uint64_t* threshold, float* keep_prob) {
+    if (!(p >= 0.0 && p <= 1.0)) return fail(RGO_EINVAL, "keep_prob must be in [0,1]");
+    const float pf = static_cast<float>(p);  // mask.hpp:59
+    if (threshold)
+        *threshold = static_cast<uint64_t>(std::llround(static_cast<double>(pf) * 4294967296.0));
+    if (keep_prob) *keep_prob = pf;
+    return RGO_OK;
+}
+
+int rgo_mask_bytes(const rgo_mask_desc* d, uint64_t* bytes) {
+    if (!d) return fail(RGO_EINVAL, "rgo_mask_bytes: null descriptor");
+    const uint64_t n = elem_count(d);
+    if (n == 0) return fail(RGO_EINVAL, "mask layout has zero elements");
+    if (bytes) *bytes = (n + 7) / 8;
+    return RGO_OK;
+}
+
+int rgo_mask_generate_ex(const rgo_mask_desc* d, uint8_t* d_bits, uint64_t bytes,
+                         const rgo_launch* launch, rgo_stream_t stream) {
+    if (int e = validate_mask(d, "rgo_mask_generate")) return e;
+    if (int e = require_device()) return e;
+    const uint64_t n = elem_count(d);
+    if (!d_bits || bytes < (n + 7) / 8)
+        return fail(RGO_EINVAL, "rgo_mask_generate: output buffer needs %llu bytes, got %llu",
+                    static_cast<unsigned long long>((n + 7) / 8),
+                    static_cast<unsigned long long>(bytes));
+    if (reinterpret_cast<uintptr_t>(d_bits) & 15)
+        return fail(RGO_EINVAL, "rgo_mask_generate: output must be 16-byte aligned");
+    rgo::MaskJob j{d_bits, n, d->seed, d->base_offset, d->threshold, static_cast<int>(d->rounds)};
+    rgo::LaunchShape ls;
+    if (launch) {
+        ls.grid = launch->grid;
+        ls.block = launch->block;
+        ls.dyn_smem = launch->dyn_smem;
+    }
+    cudaError_t e = rgo::launch_mask(j, ls, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? RGO_OK : cuda_fail(e, "rgo_mask_generate");
+}
+
+int rgo_mask_generate(const rgo_mask_desc* d, uint8_t* d_bits, uint64_t bytes,
+                      rgo_stream_t stream) {
+    return rgo_mask_generate_ex(d, d_bits, bytes, nullptr, stream);
+}
+
+int rgo_generate_mask_host(const rgo_mask_desc* d, uint8_t* h_bits, uint64_t bytes,
+                           uint32_t devices) {
+    if (int e = validate_mask(d, "generate_mask")) return e;
+    const uint64_t n = elem_count(d);
+    if (n > kMaxBits)  // mask.hpp:148-155
+        return fail(RGO_EINVAL, "generate_mask: mask needs %llu bytes, guard allows %llu bytes",
+                    static_cast<unsigned long long>((n + 7) / 8),
+                    static_cast<unsigned long long>(kMaxBits / 8));
+    const uint64_t nbytes = (n + 7) / 8;
+    if (!h_bits || bytes < nbytes)
+        return fail(RGO_EINVAL, "generate_mask: output buffer needs %llu bytes",
+                    static_cast<unsigned long long>(nbytes));
+    if (int e = require_device()) return e;
+    int ndev = rgo_device_count();
+    if (devices == 0 || devices > static_cast<uint32_t>(ndev)) devices = static_cast<uint32_t>(ndev);
+    // Shard on 16-byte (128-element) boundaries: shard r covers elements
+    // [e0, e1) and is the mask of the same layout with base_offset + e0/4,
+    // so the shards concatenate to the single-device bytes (mask.hpp:139-141).
+    const uint64_t nvec = (nbytes + 15) / 16;
+    const uint64_t per = (nvec + devices - 1) / devices;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    std::vector<int> status(devices, RGO_OK);
+    std::vector<std::string> msgs(devices);
+    auto work = [&](uint32_t r) {
+        const uint64_t v0 = r * per, v1 = std::min(nvec, v0 + per);
+        if (v0 >= v1) return;
+        const uint64_t e0 = v0 * 128, e1 = std::min(n, v1 * 128);
+        const uint64_t b0 = v0 * 16, b1 = std::min(nbytes, v1 * 16);
+        cudaSetDevice(static_cast<int>(r));
+        uint8_t* dbuf = nullptr;
+        cudaError_t ce = cudaMalloc(&dbuf, (b1 - b0 + 15) & ~uint64_t{15});
+        if (ce != cudaSuccess) {
+            status[r] = RGO_ENOMEM;
+            msgs[r] = cudaGetErrorString(ce);
+            return;
+        }
+        rgo::MaskJob j{dbuf, e1 - e0, d->seed, d->base_offset + e0 / 4, d->threshold,
+                       static_cast<int>(d->rounds)};
+        ce = rgo::launch_mask(j, rgo::LaunchShape{}, nullptr);
+        if (ce == cudaSuccess) ce = cudaMemcpy(h_bits + b0, dbuf, b1 - b0, cudaMemcpyDeviceToHost);
+        cudaFree(dbuf);
+        if (ce != cudaSuccess) {
+            status[r] = RGO_ECUDA;
+            msgs[r] = cudaGetErrorString(ce);
+        }
+    };
+    if (devices == 1) {
+        work(0);
+    } else {
+        std::vector<std::thread> pool;
+        for (uint32_t r = 0; r < devices; ++r) pool.emplace_back(work, r);
+        for (auto& t : pool) t.join();
+    }
+    cudaSetDevice(prev);
+    for (uint32_t r = 0; r < devices; ++r)
+        if (status[r] != RGO_OK)
+            return fail(status[r], "generate_mask (device %u): %s", r, msgs[r].c_str());
+    return RGO_OK;
+}
+
+int rgo_uniform_fill(uint64_t seed, uint32_t stream_id, uint64_t n, void* d_bf16, float* d_f32,
+                     rgo_stream_t stream) {
+    if (int e = require_device()) return e;
+    cudaError_t e =
+        rgo::launch_uniform_bf16(seed, stream_id, n, d_bf16, d_f32, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? RGO_OK : cuda_fail(e, "rgo_uniform_fill");
+}
+
+}  // extern "C"

@@ -1,0 +1,100 @@
+"""CPU: the C-ABI library loads, exports every function include/rgo/capi.h
+declares, validates like the reference, and refuses to compute without a GPU
+(no CPU fallback)."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+from conftest import ROOT
+
+
+def declared_symbols():
+    text = open(os.path.join(ROOT, "include", "rgo", "capi.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(rgo_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_every_declared_symbol_is_exported(rgo):
+    lib = rgo._lib.lib()
+    syms = declared_symbols()
+    assert len(syms) >= 10
+    for s in syms:
+        assert hasattr(lib, s), s
+        assert s in rgo._lib.SIGNATURES, f"{s} missing from the Python binding"
+
+
+def test_keep_threshold_via_capi(rgo):
+    lib = rgo._lib.lib()
+    t, f = C.c_uint64(), C.c_float()
+    assert lib.rgo_keep_threshold(0.9, C.byref(t), C.byref(f)) == 0
+    assert t.value == 3865470464 and abs(f.value - 0.9) < 1e-7
+    assert lib.rgo_keep_threshold(1.0, C.byref(t), None) == 0 and t.value == 1 << 32
+    assert lib.rgo_keep_threshold(1.5, C.byref(t), None) == rgo._lib.RGO_EINVAL
+    assert b"keep_prob" in lib.rgo_last_error()
+
+
+def test_threshold_python_mirror_matches_oracle(rgo, golden):
+    for p, thr in golden["thresholds"].items():
+        assert rgo.KeepThreshold(float(p)).threshold() == thr
+
+
+def test_validation_errors(rgo):
+    lib = rgo._lib.lib()
+    d = rgo._lib.mask_desc(0, 1, 1, 7, 0, 0, 1 << 31)
+    assert lib.rgo_mask_generate(d, None, 0, None) == rgo._lib.RGO_EINVAL
+    assert b"zero elements" in lib.rgo_last_error()
+    d = rgo._lib.mask_desc(1, 1, 4, 17, 0, 0, 1 << 31)
+    assert lib.rgo_mask_generate(d, None, 0, None) == rgo._lib.RGO_EINVAL
+    assert b"rounds" in lib.rgo_last_error()
+    # capacity guard (mask.hpp:148-155): message carries "bytes" and "guard"
+    with pytest.raises(ValueError) as e:
+        rgo.generate_mask(rgo.MaskLayout(1, 96, 1 << 17), rgo.KeepThreshold(0.5), 7)
+    assert "bytes" in str(e.value) and "guard" in str(e.value)
+    with pytest.raises(ValueError):
+        rgo.generate_mask(rgo.MaskLayout(1, 1, 4), rgo.KeepThreshold(0.5), 0)
+    with pytest.raises(ValueError):
+        rgo.MaskLayout(1, 2, 4).linear_index(0, 2, 0, 0)
+
+
+def test_no_cpu_fallback(rgo):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    with pytest.raises(rgo._lib.RgoError) as e:
+        rgo.generate_mask(rgo.MaskLayout(1, 1, 16, 3), rgo.KeepThreshold(0.9), 10)
+    assert e.value.code == rgo._lib.RGO_ENODEV
+
+
+def test_mask_file_roundtrip_and_errors(rgo, tmp_path, mask_blobs, golden):
+    # test_mask.cpp:172-219 with reference bits from the golden fixture
+    m = next(x for x in golden["masks"] if x["seed"] == 31337)
+    mask = rgo.DropoutMask(rgo.MaskLayout(m["batch"], m["heads"], m["seq"], m["seed"], m["base_offset"]),
+                           rgo.KeepThreshold(m["p"]).keep_prob, m["rounds"], mask_blobs[m["blob"]])
+    p = tmp_path / "m.bin"
+    rgo.save_mask(mask, p)
+    assert p.stat().st_size == 40 + (mask.layout.elem_count() + 7) // 8
+    r = rgo.load_mask(p)
+    assert r.layout == mask.layout and r.keep_prob == mask.keep_prob and r.rounds == mask.rounds
+    assert (r.bits == mask.bits).all()
+    raw = bytearray(p.read_bytes())
+    raw[0] = ord("X")
+    (tmp_path / "bad.bin").write_bytes(bytes(raw))
+    with pytest.raises(rgo._lib.RgoIOError):
+        rgo.load_mask(tmp_path / "bad.bin")
+    (tmp_path / "short.bin").write_bytes(p.read_bytes()[:-1])
+    with pytest.raises(rgo._lib.RgoIOError):
+        rgo.load_mask(tmp_path / "short.bin")
+
+
+def test_element_source_carry(rgo):
+    # test_mask.cpp:23-61
+    lay = rgo.MaskLayout(1, 2, 4)
+    assert rgo.element_source(lay, 0) == (rgo.PhiloxCounter(0, 0, 0, 0), 0)
+    assert rgo.element_source(lay, 7) == (rgo.PhiloxCounter(1, 0, 0, 0), 3)
+    with pytest.raises(ValueError):
+        rgo.element_source(lay, 32)
+    lay = rgo.MaskLayout(1, 4, 65536, 0, 0xFFFFFFFF)
+    c, lane = rgo.element_source(lay, 1 << 33)
+    assert lane == 0 and c.c1 == 1 and c.c0 == ((0xFFFFFFFF + (1 << 31)) & 0xFFFFFFFF)
