@@ -106,6 +106,48 @@ int rgo_generate_mask_host(const rgo_mask_desc* d, uint8_t* h_bits, uint64_t byt
 int rgo_uniform_fill(uint64_t seed, uint32_t stream_id, uint64_t n, void* d_bf16, float* d_f32,
                      rgo_stream_t stream);
 
+/* Dropout-mask work queue (overlap mechanism B tail / dynamic scheduling):
+ * drains vectors [*d_counter, n/128) of layout d into d_bits, claiming
+ * 32-vector chunks with atomics on d_counter (zero it before the first
+ * producer of a pass).  Requires B*nH*SQ^2 % 128 == 0 and threshold < 2^32. */
+int rgo_mask_queue_drain(const rgo_mask_desc* d, uint8_t* d_bits, uint64_t bytes,
+                         unsigned long long* d_counter, const rgo_launch* launch,
+                         rgo_stream_t stream);
+
+/* ------------------------------------------------------------------ GEMM --
+ * K2/K3: C[m, n_out] = epilogue(alpha * A[m,k] . B[n,k]^T) * out_scale on
+ * tcgen05 tensor cores (shapes: proj/include/rgo/workload.hpp:44-52).
+ * A and B are K-major (row-major [rows, k]); C row-major.  SwiGLU expects B
+ * rows interleaved per 256-row tile as [128 gate | 128 up] and writes
+ * n_out = n/2 columns.  Requirements: k*sizeof(in) % 128 == 0, 16-byte
+ * aligned pointers and leading dimensions, n % 32 == 0 (n % 256 == 0 for
+ * SwiGLU). */
+typedef enum rgo_dtype { RGO_DT_BF16 = 0, RGO_DT_E4M3 = 1 } rgo_dtype;
+typedef enum rgo_epilogue { RGO_EPI_NONE = 0, RGO_EPI_SWIGLU = 1, RGO_EPI_GELU = 2 } rgo_epilogue;
+
+typedef struct rgo_gemm_desc {
+    int32_t m, n, k;
+    int32_t in_dtype;   /* rgo_dtype of A and B */
+    int32_t out_dtype;  /* rgo_dtype of C */
+    int32_t epilogue;   /* rgo_epilogue */
+    int64_t lda, ldb, ldc; /* elements */
+    float alpha;        /* dequantisation scale of A.B (sa * sb) */
+    float out_scale;    /* multiplier before the output cast */
+    int32_t grid;       /* 0 = one persistent CTA per SM */
+    int32_t reserved;
+} rgo_gemm_desc;
+
+int rgo_gemm(const rgo_gemm_desc* g, const void* d_a, const void* d_b, void* d_c,
+             rgo_stream_t stream);
+
+/* K4: the same GEMM with co-resident RNG warps (overlap mechanism B) that
+ * drain the dropout-mask queue of layout m into d_bits while the tensor
+ * cores run.  Whatever is left when the GEMM finishes is picked up by the
+ * next rgo_gemm_with_rng on the same queue or by rgo_mask_queue_drain. */
+int rgo_gemm_with_rng(const rgo_gemm_desc* g, const void* d_a, const void* d_b, void* d_c,
+                      const rgo_mask_desc* m, uint8_t* d_bits, uint64_t bytes,
+                      unsigned long long* d_counter, rgo_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

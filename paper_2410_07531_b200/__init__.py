@@ -10,7 +10,12 @@ from .philox import (PhiloxBlock, PhiloxCounter, PhiloxKey, advance, bump_key, p
 from .mask import (DropoutMask, KeepThreshold, MaskLayout, element_source, generate_mask,
                    generate_mask_device, keep_bit_direct, load_mask, mask_bit, save_mask)
 
+from .gemm import (GemmShape, WorkloadConfig, attention_work, gemm, gemm_shapes, gemm_with_rng,
+                   mask_queue_drain, rng_elements, workload_preset)
+
 __all__ = [
+    "GemmShape", "WorkloadConfig", "attention_work", "gemm", "gemm_shapes", "gemm_with_rng",
+    "mask_queue_drain", "rng_elements", "workload_preset",
     "PhiloxBlock", "PhiloxCounter", "PhiloxKey", "advance", "bump_key", "philox_block",
     "philox_blocks", "philox_round", "DropoutMask", "KeepThreshold", "MaskLayout",
     "element_source", "generate_mask", "generate_mask_device", "keep_bit_direct", "load_mask",

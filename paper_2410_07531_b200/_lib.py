@@ -48,6 +48,16 @@ class launch(C.Structure):
     ]
 
 
+class gemm_desc(C.Structure):
+    _fields_ = [
+        ("m", C.c_int32), ("n", C.c_int32), ("k", C.c_int32),
+        ("in_dtype", C.c_int32), ("out_dtype", C.c_int32), ("epilogue", C.c_int32),
+        ("lda", C.c_int64), ("ldb", C.c_int64), ("ldc", C.c_int64),
+        ("alpha", C.c_float), ("out_scale", C.c_float),
+        ("grid", C.c_int32), ("reserved", C.c_int32),
+    ]
+
+
 # name -> (restype, argtypes).  Every symbol include/rgo/capi.h declares.
 SIGNATURES = {
     "rgo_last_error": (C.c_char_p, []),
@@ -67,6 +77,16 @@ SIGNATURES = {
     "rgo_generate_mask_host": (
         C.c_int,
         [C.POINTER(mask_desc), C.c_void_p, C.c_uint64, C.c_uint32],
+    ),
+    "rgo_mask_queue_drain": (
+        C.c_int,
+        [C.POINTER(mask_desc), C.c_void_p, C.c_uint64, C.c_void_p, C.POINTER(launch), C.c_void_p],
+    ),
+    "rgo_gemm": (C.c_int, [C.POINTER(gemm_desc), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "rgo_gemm_with_rng": (
+        C.c_int,
+        [C.POINTER(gemm_desc), C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(mask_desc), C.c_void_p,
+         C.c_uint64, C.c_void_p, C.c_void_p],
     ),
     "rgo_uniform_fill": (
         C.c_int,

@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "rgo/capi.h"
+#include "gemm.h"
 #include "rgo_internal.h"
 
 namespace {
@@ -212,6 +213,97 @@ int rgo_uniform_fill(uint64_t seed, uint32_t stream_id, uint64_t n, void* d_bf16
     cudaError_t e =
         rgo::launch_uniform_bf16(seed, stream_id, n, d_bf16, d_f32, static_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? RGO_OK : cuda_fail(e, "rgo_uniform_fill");
+}
+
+static int make_queue(const rgo_mask_desc* d, uint8_t* d_bits, uint64_t bytes,
+                      unsigned long long* d_counter, rgo::RngQueue* q, const char* fn) {
+    if (int e = validate_mask(d, fn)) return e;
+    const uint64_t n = elem_count(d);
+    if (n % 128) return fail(RGO_EINVAL, "%s: queue needs B*nH*SQ^2 %% 128 == 0", fn);
+    if (d->threshold == 0 || d->threshold >= (uint64_t{1} << 32))
+        return fail(RGO_EINVAL, "%s: queue needs 0 < threshold < 2^32 (use rgo_mask_generate)", fn);
+    if (!d_bits || bytes < n / 8 || (reinterpret_cast<uintptr_t>(d_bits) & 15))
+        return fail(RGO_EINVAL, "%s: output needs %llu bytes, 16-byte aligned", fn,
+                    static_cast<unsigned long long>(n / 8));
+    if (!d_counter) return fail(RGO_EINVAL, "%s: null queue counter", fn);
+    q->out = d_bits;
+    q->n_vec = n / 128;
+    q->base_offset = d->base_offset;
+    q->k0 = static_cast<uint32_t>(d->seed);
+    q->k1 = static_cast<uint32_t>(d->seed >> 32);
+    q->thr = static_cast<uint32_t>(d->threshold);
+    q->rounds = static_cast<int>(d->rounds);
+    q->counter = d_counter;
+    return RGO_OK;
+}
+
+int rgo_mask_queue_drain(const rgo_mask_desc* d, uint8_t* d_bits, uint64_t bytes,
+                         unsigned long long* d_counter, const rgo_launch* launch,
+                         rgo_stream_t stream) {
+    rgo::RngQueue q{};
+    if (int e = make_queue(d, d_bits, bytes, d_counter, &q, "rgo_mask_queue_drain")) return e;
+    if (int e = require_device()) return e;
+    cudaError_t ce = rgo::launch_rng_queue(q, launch ? launch->grid : 0, launch ? launch->block : 0,
+                                           launch ? launch->dyn_smem : 0,
+                                           static_cast<cudaStream_t>(stream));
+    return ce == cudaSuccess ? RGO_OK : cuda_fail(ce, "rgo_mask_queue_drain");
+}
+
+static int gemm_job(const rgo_gemm_desc* g, const void* a, const void* b, void* c, rgo::GemmJob* j) {
+    if (!g) return fail(RGO_EINVAL, "rgo_gemm: null descriptor");
+    if (g->m <= 0 || g->n <= 0 || g->k <= 0) return fail(RGO_EINVAL, "rgo_gemm: dims must be >= 1");
+    if (g->in_dtype != RGO_DT_BF16 && g->in_dtype != RGO_DT_E4M3)
+        return fail(RGO_EINVAL, "rgo_gemm: bad input dtype");
+    if (g->out_dtype != RGO_DT_BF16 && g->out_dtype != RGO_DT_E4M3)
+        return fail(RGO_EINVAL, "rgo_gemm: bad output dtype");
+    if (g->epilogue < RGO_EPI_NONE || g->epilogue > RGO_EPI_GELU)
+        return fail(RGO_EINVAL, "rgo_gemm: bad epilogue");
+    const int esz = g->in_dtype == RGO_DT_E4M3 ? 1 : 2;
+    const int osz = g->out_dtype == RGO_DT_E4M3 ? 1 : 2;
+    if ((static_cast<int64_t>(g->k) * esz) % 128)
+        return fail(RGO_EINVAL, "rgo_gemm: k*sizeof(in) must be a multiple of 128 bytes");
+    if (g->n % 32) return fail(RGO_EINVAL, "rgo_gemm: n must be a multiple of 32");
+    if (g->epilogue == RGO_EPI_SWIGLU && g->n % 256)
+        return fail(RGO_EINVAL, "rgo_gemm: SwiGLU needs n %% 256 == 0");
+    if (g->in_dtype == RGO_DT_BF16 && g->out_dtype == RGO_DT_E4M3)
+        return fail(RGO_EINVAL, "rgo_gemm: bf16 inputs produce bf16 output");
+    const int n_out = g->epilogue == RGO_EPI_SWIGLU ? g->n / 2 : g->n;
+    if (g->lda < g->k || g->ldb < g->k || g->ldc < n_out)
+        return fail(RGO_EINVAL, "rgo_gemm: leading dimension too small");
+    if (((g->lda * esz) | (g->ldb * esz) | (g->ldc * osz)) % 16)
+        return fail(RGO_EINVAL, "rgo_gemm: leading dimensions must be 16-byte multiples");
+    if (!a || !b || !c || ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b) |
+                            reinterpret_cast<uintptr_t>(c)) & 15))
+        return fail(RGO_EINVAL, "rgo_gemm: pointers must be non-null and 16-byte aligned");
+    j->fp8 = g->in_dtype == RGO_DT_E4M3;
+    j->M = g->m; j->N = g->n; j->K = g->k;
+    j->A = a; j->lda = g->lda; j->B = b; j->ldb = g->ldb; j->C = c; j->ldc = g->ldc;
+    j->epi = g->epilogue;
+    j->out = g->out_dtype == RGO_DT_E4M3 ? rgo_gk::OUT_E4M3 : rgo_gk::OUT_BF16;
+    j->alpha = g->alpha; j->out_scale = g->out_scale; j->grid = g->grid; j->rng = nullptr;
+    return RGO_OK;
+}
+
+int rgo_gemm(const rgo_gemm_desc* g, const void* d_a, const void* d_b, void* d_c,
+             rgo_stream_t stream) {
+    rgo::GemmJob j{};
+    if (int e = gemm_job(g, d_a, d_b, d_c, &j)) return e;
+    if (int e = require_device()) return e;
+    cudaError_t ce = rgo::launch_gemm(j, static_cast<cudaStream_t>(stream));
+    return ce == cudaSuccess ? RGO_OK : cuda_fail(ce, "rgo_gemm");
+}
+
+int rgo_gemm_with_rng(const rgo_gemm_desc* g, const void* d_a, const void* d_b, void* d_c,
+                      const rgo_mask_desc* m, uint8_t* d_bits, uint64_t bytes,
+                      unsigned long long* d_counter, rgo_stream_t stream) {
+    rgo::GemmJob j{};
+    if (int e = gemm_job(g, d_a, d_b, d_c, &j)) return e;
+    rgo::RngQueue q{};
+    if (int e = make_queue(m, d_bits, bytes, d_counter, &q, "rgo_gemm_with_rng")) return e;
+    if (int e = require_device()) return e;
+    j.rng = &q;
+    cudaError_t ce = rgo::launch_gemm(j, static_cast<cudaStream_t>(stream));
+    return ce == cudaSuccess ? RGO_OK : cuda_fail(ce, "rgo_gemm_with_rng");
 }
 
 }  // extern "C"

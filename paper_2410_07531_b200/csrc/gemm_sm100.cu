@@ -1,0 +1,339 @@
+// gemm_sm100.cu -- K2/K3: persistent, warp-specialised tcgen05 GEMM for the
+// transformer-block projections whose shapes the reference defines
+// (proj/include/rgo/workload.hpp:44-52: QKV, Proj, FFN1, FFN2).
+//
+//   C[M, N] = epilogue( alpha * A[M, K] . B[N, K]^T )      (both K-major)
+//
+// * A, B: E4M3 (kind::f8f6f4) or BF16 (kind::f16), fp32 accumulate in TMEM.
+// * Tile 128 x 256 x (128 bytes of K); 4-stage TMA -> smem ring (48 KiB/stage,
+//   SWIZZLE_128B), mbarrier full/empty pipeline.
+// * Warp roles (192 threads): warp 0 = TMA producer, warp 1 = MMA issuer
+//   (one thread issues tcgen05.mma), warps 2-5 = epilogue (TMEM -> registers ->
+//   scale/activation -> bf16 or e4m3 -> global).  Two 256-column TMEM
+//   accumulators (512 columns) so the epilogue of tile i overlaps the MMAs of
+//   tile i+1.
+// * Persistent grid = #SMs, grouped rasterisation (16 M-blocks per group) so
+//   the concurrently running tiles share A rows and B columns in L2.
+// * Optional co-resident RNG warps (overlap mechanism B): extra warps that
+//   drain the dropout-mask work queue (csrc/rng_queue.cuh) while the tensor
+//   core runs, using the registers TMEM frees.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp8.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "gemm.h"
+#include "philox.cuh"
+#include "rgo_internal.h"
+#include "rng_queue.cuh"
+#include "sm100_ptx.cuh"
+#include "tma_host.h"
+
+namespace rgo_gk {
+
+constexpr int BM = 128;
+constexpr int BN = 256;
+constexpr int BKB = 128;  // K bytes per stage (64 bf16 / 128 e4m3)
+constexpr int STAGES = 4;
+constexpr int A_BYTES = BM * BKB;
+constexpr int B_BYTES = BN * BKB;
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int GROUP_M = 16;
+constexpr int CORE_THREADS = 192;
+constexpr uint32_t TMEM_COLS = 512;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+
+struct Params {
+    int M, N, K;          // N = rows of B; K in elements
+    int tiles_m, tiles_n;
+    void* C;
+    long long ldc;        // elements
+    int n_out;            // output columns (N, or N/2 for SwiGLU)
+    float alpha;          // dequant scale (sa * sb)
+    float out_scale;      // multiply before the output cast (fp8 quantisation)
+    // co-resident RNG (mechanism B)
+    rgo::RngQueue rng;
+};
+
+__device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, int& mb, int& nb) {
+    const int per_group = GROUP_M * tiles_n;
+    const int group = tile / per_group;
+    const int first_m = group * GROUP_M;
+    const int gsize = min(tiles_m - first_m, GROUP_M);
+    const int local = tile - group * per_group;
+    mb = first_m + local % gsize;
+    nb = local / gsize;
+}
+
+__device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
+__device__ __forceinline__ float gelu_tanh(float x) {
+    const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+    return 0.5f * x * (1.0f + tanhf(k0 * (x + k1 * x * x * x)));
+}
+
+template <int OUT>
+__device__ __forceinline__ void store32(void* C, long long ldc, int row, int col, const float (&v)[32]) {
+    if constexpr (OUT == OUT_BF16) {
+        uint32_t packed[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+            packed[i] = *reinterpret_cast<uint32_t*>(&h);
+        }
+        uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(C) + row * ldc + col);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
+    } else {
+        uint32_t packed[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const __nv_fp8x2_storage_t lo =
+                __nv_cvt_float2_to_fp8x2(make_float2(v[4 * i], v[4 * i + 1]), __NV_SATFINITE, __NV_E4M3);
+            const __nv_fp8x2_storage_t hi =
+                __nv_cvt_float2_to_fp8x2(make_float2(v[4 * i + 2], v[4 * i + 3]), __NV_SATFINITE, __NV_E4M3);
+            packed[i] = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
+        }
+        uint4* dst = reinterpret_cast<uint4*>(static_cast<uint8_t*>(C) + row * ldc + col);
+        dst[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+        dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+    }
+}
+
+template <bool FP8, int EPI, int OUT, int RNG_WARPS>
+__global__ void __launch_bounds__(CORE_THREADS + 32 * RNG_WARPS, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const Params p) {
+    using namespace sm100;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t{1023});
+    uint8_t* smA = smem;
+    uint8_t* smB = smem + STAGES * A_BYTES;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + STAGES;
+    uint64_t* tfull = bars + 2 * STAGES;
+    uint64_t* tempty = bars + 2 * STAGES + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+    volatile int* gemm_done = reinterpret_cast<volatile int*>(tmem_slot + 1);
+
+    const uint32_t warp = warp_id(), lane = lane_id();
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(smem_u32(&full[s]), 1);
+            mbar_init(smem_u32(&empty[s]), 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(smem_u32(&tfull[a]), 1);
+            mbar_init(smem_u32(&tempty[a]), 4);
+        }
+        *gemm_done = 0;
+        fence_mbar_init();
+        tma_prefetch_desc(&tmA);
+        tma_prefetch_desc(&tmB);
+    }
+    if (warp == 1) tmem_alloc<TMEM_COLS>(smem_u32(tmem_slot));
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    const int num_tiles = p.tiles_m * p.tiles_n;
+    const int kblocks = (p.K * (FP8 ? 1 : 2)) / BKB;
+    const int bk_elems = FP8 ? BKB : BKB / 2;
+    constexpr uint32_t IDESC = FP8 ? idesc_make(0, 0, BM, BN, 0, 0) : idesc_make(1, 1, BM, BN, 0, 0);
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---------------- TMA producer
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                int mb, nb;
+                tile_coords(tile, p.tiles_m, p.tiles_n, mb, nb);
+                for (int kb = 0; kb < kblocks; ++kb) {
+                    mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+                    const uint32_t fb = smem_u32(&full[stage]);
+                    mbar_arrive_expect_tx(fb, STAGE_BYTES);
+                    tma_load_2d(smem_u32(smA + stage * A_BYTES), &tmA, fb, kb * bk_elems, mb * BM);
+                    tma_load_2d(smem_u32(smB + stage * B_BYTES), &tmB, fb, kb * bk_elems, nb * BN);
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---------------- MMA issuer
+            int stage = 0;
+            uint32_t phase = 0, acc = 0, acc_phase = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                mbar_wait(smem_u32(&tempty[acc]), acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem_base + acc * BN;
+                for (int kb = 0; kb < kblocks; ++kb) {
+                    mbar_wait(smem_u32(&full[stage]), phase);
+                    tc_fence_after();
+                    const uint64_t ad = desc_kmajor_sw128(smem_u32(smA + stage * A_BYTES));
+                    const uint64_t bd = desc_kmajor_sw128(smem_u32(smB + stage * B_BYTES));
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {  // 4 x 32 bytes of K per stage
+                        const uint32_t acc_flag = (kb | k) != 0;
+                        if constexpr (FP8)
+                            mma_f8_ss(d, ad + 2 * k, bd + 2 * k, IDESC, acc_flag);
+                        else
+                            mma_f16_ss(d, ad + 2 * k, bd + 2 * k, IDESC, acc_flag);
+                    }
+                    tc_commit(smem_u32(&empty[stage]));
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                tc_commit(smem_u32(&tfull[acc]));
+                acc ^= 1;
+                if (acc == 0) acc_phase ^= 1;
+            }
+        }
+        __syncwarp();
+    } else if (warp < CORE_THREADS / 32) {  // ---------------- epilogue warps 2..5
+        const uint32_t q = warp & 3;  // TMEM lane quarter this warp may access
+        const int row_in_tile = q * 32 + lane;
+        uint32_t acc = 0, acc_phase = 0;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            int mb, nb;
+            tile_coords(tile, p.tiles_m, p.tiles_n, mb, nb);
+            mbar_wait(smem_u32(&tfull[acc]), acc_phase);
+            tc_fence_after();
+            const int row = mb * BM + row_in_tile;
+            const uint32_t tbase = tmem_base + ((q * 32) << 16) + acc * BN;
+            if constexpr (EPI == EPI_SWIGLU) {
+#pragma unroll 1
+                for (int c = 0; c < 4; ++c) {  // gate cols [32c,32c+32), up cols 128 + [32c, ...)
+                    uint32_t g[32], u[32];
+                    tmem_ld32(tbase + c * 32, g);
+                    tmem_ld32(tbase + 128 + c * 32, u);
+                    tmem_ld_wait();
+                    float v[32];
+#pragma unroll
+                    for (int i = 0; i < 32; ++i)
+                        v[i] = silu(__uint_as_float(g[i]) * p.alpha) * (__uint_as_float(u[i]) * p.alpha) *
+                               p.out_scale;
+                    const int col = nb * (BN / 2) + c * 32;
+                    if (row < p.M && col < p.n_out) store32<OUT>(p.C, p.ldc, row, col, v);
+                }
+            } else {
+#pragma unroll 1
+                for (int c = 0; c < BN / 32; ++c) {
+                    uint32_t r[32];
+                    tmem_ld32(tbase + c * 32, r);
+                    tmem_ld_wait();
+                    float v[32];
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        float x = __uint_as_float(r[i]) * p.alpha;
+                        if constexpr (EPI == EPI_GELU) x = gelu_tanh(x);
+                        v[i] = x * p.out_scale;
+                    }
+                    const int col = nb * BN + c * 32;
+                    if (row < p.M && col < p.n_out) store32<OUT>(p.C, p.ldc, row, col, v);
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&tempty[acc]));
+            acc ^= 1;
+            if (acc == 0) acc_phase ^= 1;
+        }
+    } else {
+        // ---------------- co-resident RNG warps (mechanism B)
+        if constexpr (RNG_WARPS > 0) rgo::rng_queue_drain(p.rng, gemm_done, 4);
+    }
+    if constexpr (RNG_WARPS > 0) {
+        // GEMM roles signal completion so RNG warps stop pulling new chunks.
+        if (warp >= 2 && warp < CORE_THREADS / 32) {
+            // epilogue warps finish last among GEMM roles
+            __syncwarp();
+            if (lane == 0) atomicAdd(const_cast<int*>(gemm_done), 1);
+        }
+    }
+    __syncthreads();
+    if (warp == 1) tmem_dealloc<TMEM_COLS>(tmem_base);
+}
+
+template <bool FP8, int EPI, int OUT, int RNG_WARPS>
+static cudaError_t launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, int grid,
+                            cudaStream_t s) {
+    auto k = gemm_kernel<FP8, EPI, OUT, RNG_WARPS>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    k<<<grid, CORE_THREADS + 32 * RNG_WARPS, SMEM_BYTES, s>>>(ta, tb, p);
+    return cudaGetLastError();
+}
+
+}  // namespace rgo_gk
+
+namespace rgo {
+
+cudaError_t launch_gemm(const GemmJob& j, cudaStream_t s) {
+    using namespace rgo_gk;
+    const bool fp8 = j.fp8;
+    const size_t esz = fp8 ? 1 : 2;
+    if ((j.K * esz) % BKB != 0 || j.M <= 0 || j.N <= 0) return cudaErrorInvalidValue;
+    if (j.epi == EPI_SWIGLU && j.N % BN != 0) return cudaErrorInvalidValue;
+    const CUtensorMapDataType dt = fp8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+    CUtensorMap ta, tb;
+    {
+        const uint64_t dims[2] = {static_cast<uint64_t>(j.K), static_cast<uint64_t>(j.M)};
+        const uint64_t strides[1] = {static_cast<uint64_t>(j.lda) * esz};
+        const uint32_t box[2] = {static_cast<uint32_t>(BKB / esz), BM};
+        if (!make_tmap(&ta, j.A, dt, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B))
+            return cudaErrorInvalidValue;
+    }
+    {
+        const uint64_t dims[2] = {static_cast<uint64_t>(j.K), static_cast<uint64_t>(j.N)};
+        const uint64_t strides[1] = {static_cast<uint64_t>(j.ldb) * esz};
+        const uint32_t box[2] = {static_cast<uint32_t>(BKB / esz), BN};
+        if (!make_tmap(&tb, j.B, dt, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B))
+            return cudaErrorInvalidValue;
+    }
+    Params p{};
+    p.M = j.M;
+    p.N = j.N;
+    p.K = j.K;
+    p.tiles_m = (j.M + BM - 1) / BM;
+    p.tiles_n = (j.N + BN - 1) / BN;
+    p.C = j.C;
+    p.ldc = j.ldc;
+    p.n_out = j.epi == EPI_SWIGLU ? j.N / 2 : j.N;
+    p.alpha = j.alpha;
+    p.out_scale = j.out_scale;
+    if (j.rng) p.rng = *j.rng;
+    const int tiles = p.tiles_m * p.tiles_n;
+    int grid = j.grid > 0 ? j.grid : num_sms();
+    if (grid > tiles) grid = tiles;
+    const bool rng = j.rng != nullptr;
+#define RGO_G(F, E, O)                                                         \
+    if (fp8 == F && j.epi == E && j.out == O)                                  \
+        return rng ? launch_t<F, E, O, RNG_WARPS_IN_GEMM>(ta, tb, p, grid, s)  \
+                   : launch_t<F, E, O, 0>(ta, tb, p, grid, s);
+    RGO_G(true, EPI_NONE, OUT_BF16)
+    RGO_G(true, EPI_NONE, OUT_E4M3)
+    RGO_G(true, EPI_SWIGLU, OUT_E4M3)
+    RGO_G(true, EPI_SWIGLU, OUT_BF16)
+    RGO_G(true, EPI_GELU, OUT_E4M3)
+    RGO_G(false, EPI_NONE, OUT_BF16)
+    RGO_G(false, EPI_SWIGLU, OUT_BF16)
+    RGO_G(false, EPI_GELU, OUT_BF16)
+#undef RGO_G
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace rgo

@@ -81,14 +81,18 @@ __device__ __forceinline__ uint32_t keep32(uint64_t ctr0, uint32_t k0, uint32_t 
     return acc;
 }
 
-// acc = 2*acc + (w >= thr) in two ALU ops (IADD3 with carry-out, IADD3.X):
+// acc = 2*acc + (w >= thr) in two ALU-pipe ops (IADD3 carry-out, IADD3.X):
 // w - thr borrows exactly when w < thr, i.e. the carry-out is the DROP bit.
-// Callers feed elements high-to-low and invert once per 32-bit word.
-__device__ __forceinline__ uint32_t push_drop_bit(uint32_t acc, uint32_t w, uint32_t thr) {
+// `zero` is an opaque 0 (kernel parameter): the third addend keeps ptxas
+// from lowering the carry-add to IMAD.X, which would land on the fma-heavy
+// pipe that the IMAD.WIDE multiplies already saturate.  Callers feed
+// elements high-to-low and invert once per 32-bit word.
+__device__ __forceinline__ uint32_t push_drop_bit(uint32_t acc, uint32_t w, uint32_t thr,
+                                                  uint32_t zero) {
     uint32_t r;
-    asm("{\n\t.reg .u32 t;\n\tsub.cc.u32 t, %1, %2;\n\taddc.u32 %0, %3, %3;\n\t}"
+    asm("{\n\t.reg .u32 t;\n\tsub.cc.u32 t, %1, %2;\n\taddc.u32 t, %3, %3;\n\tadd.u32 %0, t, %4;\n\t}"
         : "=r"(r)
-        : "r"(w), "r"(thr), "r"(acc));
+        : "r"(w), "r"(thr), "r"(acc), "r"(zero));
     return r;
 }
 
@@ -99,17 +103,17 @@ __device__ __forceinline__ uint32_t push_drop_bit(uint32_t acc, uint32_t w, uint
 // chain above (2 ops/element).  Bit-identical to keep32().
 template <int R>
 __device__ __forceinline__ uint32_t keep32_nowrap(uint32_t lo, uint32_t hi, uint32_t k0,
-                                                  uint32_t k1, uint32_t thr) {
+                                                  uint32_t k1, uint32_t thr, uint32_t zero) {
     uint4 w[8];
 #pragma unroll
     for (int b = 0; b < 8; ++b) w[b] = philox<R>(lo + b, hi, 0u, 0u, k0, k1);
     uint32_t drop = 0;
 #pragma unroll
     for (int b = 7; b >= 0; --b) {  // element 32q+4b+lane -> bit 4b+lane
-        drop = push_drop_bit(drop, w[b].w, thr);
-        drop = push_drop_bit(drop, w[b].z, thr);
-        drop = push_drop_bit(drop, w[b].y, thr);
-        drop = push_drop_bit(drop, w[b].x, thr);
+        drop = push_drop_bit(drop, w[b].w, thr, zero);
+        drop = push_drop_bit(drop, w[b].z, thr, zero);
+        drop = push_drop_bit(drop, w[b].y, thr, zero);
+        drop = push_drop_bit(drop, w[b].x, thr, zero);
     }
     return ~drop;
 }

@@ -34,7 +34,7 @@ __device__ __forceinline__ void st_v4_streaming(uint8_t* p, uint32_t a, uint32_t
 template <int R>
 __global__ void __launch_bounds__(256) rng_mask_kernel(uint8_t* __restrict__ out, uint64_t n_vec,
                                                        uint64_t base_offset, uint32_t k0,
-                                                       uint32_t k1, uint32_t thr) {
+                                                       uint32_t k1, uint32_t thr, uint32_t zero) {
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
     for (uint64_t v = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < n_vec;
          v += stride) {
@@ -42,10 +42,10 @@ __global__ void __launch_bounds__(256) rng_mask_kernel(uint8_t* __restrict__ out
         const uint32_t lo = static_cast<uint32_t>(ctr), hi = static_cast<uint32_t>(ctr >> 32);
         uint32_t w0, w1, w2, w3;
         if (lo <= 0xFFFFFFFFu - 31u) {  // no carry into c1 inside this unit
-            w0 = keep32_nowrap<R>(lo + 0, hi, k0, k1, thr);
-            w1 = keep32_nowrap<R>(lo + 8, hi, k0, k1, thr);
-            w2 = keep32_nowrap<R>(lo + 16, hi, k0, k1, thr);
-            w3 = keep32_nowrap<R>(lo + 24, hi, k0, k1, thr);
+            w0 = keep32_nowrap<R>(lo + 0, hi, k0, k1, thr, zero);
+            w1 = keep32_nowrap<R>(lo + 8, hi, k0, k1, thr, zero);
+            w2 = keep32_nowrap<R>(lo + 16, hi, k0, k1, thr, zero);
+            w3 = keep32_nowrap<R>(lo + 24, hi, k0, k1, thr, zero);
         } else {
             w0 = keep32<R>(ctr + 0, k0, k1, thr);
             w1 = keep32<R>(ctr + 8, k0, k1, thr);
@@ -99,7 +99,7 @@ __global__ void mask_fill_kernel(uint8_t* __restrict__ out, uint64_t n, uint8_t 
 template <int R>
 static cudaError_t launch_r(uint8_t* out, uint64_t n_vec, uint64_t base, uint32_t k0, uint32_t k1,
                             uint32_t thr, const rgo::LaunchShape& ls, cudaStream_t s) {
-    rng_mask_kernel<R><<<ls.grid, ls.block, ls.dyn_smem, s>>>(out, n_vec, base, k0, k1, thr);
+    rng_mask_kernel<R><<<ls.grid, ls.block, ls.dyn_smem, s>>>(out, n_vec, base, k0, k1, thr, 0u);
     return cudaGetLastError();
 }
 
@@ -183,4 +183,42 @@ cudaError_t launch_mask(const MaskJob& j, const LaunchShape& shape_in, cudaStrea
     return cudaSuccess;
 }
 
+}  // namespace rgo
+
+// ------------------------------------------------------------------------
+// Queue kernel: drains the shared dropout-mask work queue (rng_queue.cuh).
+// Used as the tail after GEMM-resident RNG warps (mechanism B) and as a
+// dynamically scheduled stand-alone generator.
+#include "rng_queue.cuh"
+
+namespace rgo_dev {
+template <int R>
+__global__ void __launch_bounds__(256) rng_queue_kernel(const rgo::RngQueue q) {
+    rgo::rng_drain_r<R>(q, nullptr, 0);
+}
+}  // namespace rgo_dev
+
+namespace rgo {
+cudaError_t launch_rng_queue(const RngQueue& q, unsigned grid, unsigned block, size_t dyn_smem,
+                             cudaStream_t s) {
+    if (block == 0) block = 256;
+    if (grid == 0) grid = static_cast<unsigned>(num_sms()) * 3;
+    switch (q.rounds) {
+#define RGO_CASE(R)                                                                  \
+    case R:                                                                          \
+        if (dyn_smem > 48 * 1024)                                                    \
+            cudaFuncSetAttribute(rgo_dev::rng_queue_kernel<R>,                       \
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,        \
+                                 static_cast<int>(dyn_smem));                        \
+        rgo_dev::rng_queue_kernel<R><<<grid, block, dyn_smem, s>>>(q);               \
+        break;
+        RGO_CASE(1) RGO_CASE(2) RGO_CASE(3) RGO_CASE(4) RGO_CASE(5) RGO_CASE(6) RGO_CASE(7)
+        RGO_CASE(8) RGO_CASE(9) RGO_CASE(10) RGO_CASE(11) RGO_CASE(12) RGO_CASE(13)
+        RGO_CASE(14) RGO_CASE(15) RGO_CASE(16)
+#undef RGO_CASE
+        default:
+            return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
 }  // namespace rgo

@@ -1,0 +1,59 @@
+// rng_queue.cuh -- dropout-mask work queue (overlap mechanism B).
+// Warps claim 32-vector chunks (one 128-element vector per lane) from a
+// global counter; the same device routine runs inside the GEMM CTAs
+// (co-resident RNG warps, until the GEMM's epilogue warps finish) and in the
+// tail kernel that drains whatever the GEMMs left.  Bits are identical to K1:
+// vector v = elements [128v, 128v+128), counter base + 32v.
+#pragma once
+#include <cstdint>
+
+#include "gemm.h"
+#include "philox.cuh"
+
+namespace rgo {
+
+template <int R>
+__device__ __forceinline__ void rng_vector(const RngQueue& q, uint64_t v) {
+    const uint64_t ctr = q.base_offset + v * 32;
+    const uint32_t lo = static_cast<uint32_t>(ctr), hi = static_cast<uint32_t>(ctr >> 32);
+    uint32_t w0, w1, w2, w3;
+    if (lo <= 0xFFFFFFFFu - 31u) {
+        w0 = rgo_dev::keep32_nowrap<R>(lo + 0, hi, q.k0, q.k1, q.thr, 0u);
+        w1 = rgo_dev::keep32_nowrap<R>(lo + 8, hi, q.k0, q.k1, q.thr, 0u);
+        w2 = rgo_dev::keep32_nowrap<R>(lo + 16, hi, q.k0, q.k1, q.thr, 0u);
+        w3 = rgo_dev::keep32_nowrap<R>(lo + 24, hi, q.k0, q.k1, q.thr, 0u);
+    } else {
+        w0 = rgo_dev::keep32<R>(ctr + 0, q.k0, q.k1, q.thr);
+        w1 = rgo_dev::keep32<R>(ctr + 8, q.k0, q.k1, q.thr);
+        w2 = rgo_dev::keep32<R>(ctr + 16, q.k0, q.k1, q.thr);
+        w3 = rgo_dev::keep32<R>(ctr + 24, q.k0, q.k1, q.thr);
+    }
+    uint8_t* p = q.out + v * 16;
+    asm volatile("st.global.cs.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(w0), "r"(w1), "r"(w2), "r"(w3)
+                 : "memory");
+}
+
+// Drain until the queue is empty or (*stop >= stop_at) is observed.
+template <int R>
+__device__ __forceinline__ void rng_drain_r(const RngQueue& q, const volatile int* stop, int stop_at) {
+    const uint32_t lane = threadIdx.x & 31;
+    while (true) {
+        if (stop && *stop >= stop_at) break;
+        unsigned long long start = 0;
+        if (lane == 0) start = atomicAdd(q.counter, 32ull);
+        start = __shfl_sync(0xffffffffu, start, 0);
+        if (start >= q.n_vec) break;
+        const uint64_t v = start + lane;
+        if (v < q.n_vec) rng_vector<R>(q, v);
+    }
+}
+
+__device__ __forceinline__ void rng_queue_drain(const RngQueue& q, const volatile int* stop, int stop_at = 4) {
+    if (q.rounds == 10)
+        rng_drain_r<10>(q, stop, stop_at);
+    else if (q.rounds == 7)
+        rng_drain_r<7>(q, stop, stop_at);
+    // other round counts are served by the tail kernel (rng_queue_kernel)
+}
+
+}  // namespace rgo
