@@ -148,6 +148,44 @@ int rgo_gemm_with_rng(const rgo_gemm_desc* g, const void* d_a, const void* d_b, 
                       const rgo_mask_desc* m, uint8_t* d_bits, uint64_t bytes,
                       unsigned long long* d_counter, rgo_stream_t stream);
 
+/* ------------------------------------------------------------- attention --
+ * K5/K6: flash-attention forward with dropout on tcgen05 (replaces
+ * attn_detail::forward_impl, proj/include/rgo/ref_attention.hpp:56-92).
+ * Tensors are bf16 [batch, heads, seq, head_dim] views with element strides
+ * for batch/head/position and a contiguous head dimension: the reference's
+ * slice-major layout (stride_h = seq*head_dim) and the token-major QKV GEMM
+ * output ([B*S, 3*H], stride_s = 3*H) are both expressible. */
+typedef enum rgo_mask_source {
+    RGO_MASK_NONE = 0,   /* attention_forward (ref_attention.hpp:108-110) */
+    RGO_MASK_BITS = 1,   /* attention_dropout_decoupled: read d_bits (:129-146) */
+    RGO_MASK_PHILOX = 2  /* attention_dropout_fused: Philox inline (:114-126) */
+} rgo_mask_source;
+
+typedef struct rgo_tensor4 {
+    const void* ptr;
+    int64_t stride_b, stride_h, stride_s; /* elements */
+} rgo_tensor4;
+
+typedef struct rgo_attn_desc {
+    uint32_t batch, heads, seq, head_dim; /* head_dim in {64, 128} */
+    float scale;          /* softmax scale; 0 = 1/sqrt(head_dim) (ref_attention.hpp:33) */
+    int32_t mask_source;  /* rgo_mask_source */
+    double keep_prob;     /* (0,1]; used as float like the reference (:120, :125) */
+    uint64_t seed;        /* PHILOX: mask layout (batch*heads slices) seed */
+    uint64_t base_offset; /* PHILOX: counter of element 0 */
+    uint32_t rounds;      /* PHILOX: [1,16] */
+    uint32_t reserved;
+} rgo_attn_desc;
+
+/* O = softmax(Q K^T * scale) with dropout (denominator over all keys, kept
+ * weights / keep_prob), written to o (bf16, same view convention).  d_bits
+ * (MASK_BITS) is the packed mask in the reference layout for batch*heads
+ * slices of seq x seq, >= ceil(B*nH*SQ^2/8) bytes.  d_lse (optional):
+ * float [batch*heads*seq] natural-log row logsumexp for the backward pass. */
+int rgo_attn_fwd(const rgo_attn_desc* a, const rgo_tensor4* q, const rgo_tensor4* k,
+                 const rgo_tensor4* v, const uint8_t* d_bits, uint64_t bits_bytes,
+                 const rgo_tensor4* o, float* d_lse, rgo_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

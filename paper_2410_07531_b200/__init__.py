@@ -10,10 +10,16 @@ from .philox import (PhiloxBlock, PhiloxCounter, PhiloxKey, advance, bump_key, p
 from .mask import (DropoutMask, KeepThreshold, MaskLayout, element_source, generate_mask,
                    generate_mask_device, keep_bit_direct, load_mask, mask_bit, save_mask)
 
+from .ref_attention import (AttentionInput, AttentionOutput, EquivCase, EquivResult, attention_dropout_decoupled,
+                            attention_dropout_fused, attention_forward, attn_fwd, default_equiv_grid,
+                            random_attention_input, run_equiv_suite)
 from .gemm import (GemmShape, WorkloadConfig, attention_work, gemm, gemm_shapes, gemm_with_rng,
                    mask_queue_drain, rng_elements, workload_preset)
 
 __all__ = [
+    "AttentionInput", "AttentionOutput", "EquivCase", "EquivResult", "attention_dropout_decoupled",
+    "attention_dropout_fused", "attention_forward", "attn_fwd", "default_equiv_grid", "random_attention_input",
+    "run_equiv_suite",
     "GemmShape", "WorkloadConfig", "attention_work", "gemm", "gemm_shapes", "gemm_with_rng",
     "mask_queue_drain", "rng_elements", "workload_preset",
     "PhiloxBlock", "PhiloxCounter", "PhiloxKey", "advance", "bump_key", "philox_block",

@@ -58,6 +58,18 @@ class gemm_desc(C.Structure):
     ]
 
 
+class tensor4(C.Structure):
+    _fields_ = [("ptr", C.c_void_p), ("stride_b", C.c_int64), ("stride_h", C.c_int64), ("stride_s", C.c_int64)]
+
+
+class attn_desc(C.Structure):
+    _fields_ = [
+        ("batch", C.c_uint32), ("heads", C.c_uint32), ("seq", C.c_uint32), ("head_dim", C.c_uint32),
+        ("scale", C.c_float), ("mask_source", C.c_int32), ("keep_prob", C.c_double),
+        ("seed", C.c_uint64), ("base_offset", C.c_uint64), ("rounds", C.c_uint32), ("reserved", C.c_uint32),
+    ]
+
+
 # name -> (restype, argtypes).  Every symbol include/rgo/capi.h declares.
 SIGNATURES = {
     "rgo_last_error": (C.c_char_p, []),
@@ -87,6 +99,11 @@ SIGNATURES = {
         C.c_int,
         [C.POINTER(gemm_desc), C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(mask_desc), C.c_void_p,
          C.c_uint64, C.c_void_p, C.c_void_p],
+    ),
+    "rgo_attn_fwd": (
+        C.c_int,
+        [C.POINTER(attn_desc), C.POINTER(tensor4), C.POINTER(tensor4), C.POINTER(tensor4), C.c_void_p,
+         C.c_uint64, C.POINTER(tensor4), C.c_void_p, C.c_void_p],
     ),
     "rgo_uniform_fill": (
         C.c_int,

@@ -1,0 +1,59 @@
+// attn.h -- internal attention launch interface.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace rgo_attn {
+enum { MASK_NONE = 0, MASK_BITS = 1, MASK_PHILOX = 2 };
+
+struct AttnParams {
+    int B, H, S;
+    int n_pairs;             // ceil(S / 256): CTAs per (b, h)
+    float scale_log2;        // log2(e) / sqrt(head_dim)
+    float keep_prob;         // float keep probability (1 for no dropout)
+    const uint8_t* bits;     // MASK_BITS: packed mask, reference layout
+    uint64_t bits_bytes;
+    int bits_aligned;        // SQ % 128 == 0 and 16-byte aligned bits
+    uint32_t k0, k1;         // MASK_PHILOX: key
+    uint64_t base_offset;
+    uint32_t thr;            // threshold < 2^32
+    int rounds;
+    void* O;                 // bf16 output rows
+    long long o_sb, o_sh, o_ss;  // element strides of batch, head, position
+    float* lse;              // natural-log LSE per (slice, row), or null
+};
+}  // namespace rgo_attn
+
+namespace rgo {
+
+// A bf16 [B, nH, S, HD] view with arbitrary (batch, head, position) strides in
+// elements; the head dimension is contiguous.  Covers both the reference
+// layout (slice-major, ref_attention.hpp:20-31) and the token-major QKV GEMM
+// output ([B*S, 3*H] with a column offset per Q/K/V).
+struct AttnTensor {
+    const void* ptr;
+    long long sb, sh, ss;
+};
+struct AttnOut {
+    void* ptr;
+    long long sb, sh, ss;
+};
+
+struct AttnJob {
+    int B, H, S, HD;         // HD in {64, 128}
+    float scale;             // 1/sqrt(true head_dim)
+    AttnTensor q, k, v;
+    AttnOut o;
+    float* lse;
+    int mode;                // rgo_attn::MASK_*
+    float keep_prob;
+    const uint8_t* bits;
+    uint64_t bits_bytes;
+    uint64_t seed, base_offset, threshold;
+    int rounds;
+};
+
+cudaError_t launch_attn_fwd(const AttnJob& j, cudaStream_t s);
+
+}  // namespace rgo

@@ -1,0 +1,450 @@
+// attn_fwd_sm100.cu -- K5/K6: Blackwell flash-attention forward with dropout.
+//
+// Replaces attn_detail::forward_impl (proj/include/rgo/ref_attention.hpp:56-92)
+// for attention_forward / attention_dropout_fused / attention_dropout_decoupled
+// (:108-146).  Same semantics as the reference:
+//   * softmax denominator over ALL keys, before dropout (:78-82),
+//   * kept weights scaled by 1/keep_prob with keep_prob the float value (:85, :125),
+//   * keep bit of (slice s, row i, col j) = element (s*SQ + i)*SQ + j of the
+//     global mask layout (mask.hpp:35-39, ref_attention.hpp:141-143).
+// One kernel template, MaskSource switch:
+//   MASK_NONE    plain forward (attention_forward),
+//   MASK_BITS    reads 16 B of the precomputed bitmask per row per 128-key tile
+//                (the paper's decoupled path, K5),
+//   MASK_PHILOX  regenerates the keep bits inline with Philox-R (the
+//                conventional fused baseline, K6; bit-identical keep decisions).
+//
+// Structure (per CTA: one (b, h) slice x 256 query rows = two 128-row Q tiles):
+//   warp 0      TMA producer: Q once, K/V 128-key tiles through 2-stage rings
+//   warp 1      MMA issuer: S_w = Q_w K^T (SS, bf16 -> fp32 TMEM) and
+//               O_w += P_w V (TS: P from TMEM as bf16, V MN-major from smem)
+//   warps 2-5   softmax for Q tile 0 (one thread per row), warps 6-9 tile 1:
+//               TMEM S -> online softmax (exp2, lazy rescale when the running
+//               max grows by > 8) -> dropout -> P (bf16) back into S's columns.
+// TMEM: S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512) fp32 columns; P_w
+// overwrites the first 64 columns of S_w (bf16 pairs).  tcgen05.mma executes
+// in issue order, so S_w(j+1) is written only after O_w += P_w(j) V(j) read P.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "attn.h"
+#include "philox.cuh"
+#include "rgo_internal.h"
+#include "sm100_ptx.cuh"
+#include "tma_host.h"
+
+namespace rgo_attn {
+
+using namespace sm100;
+
+constexpr int BQ = 128;  // rows per Q tile (one softmax warpgroup)
+constexpr int BKV = 128;
+constexpr int KV_STAGES = 2;
+constexpr int THREADS = 320;
+constexpr uint32_t TMEM_COLS = 512;
+constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
+
+template <int HD>
+struct Smem {
+    static constexpr int CHUNK = 128 * 128;            // one 64-dH (128 B) column block of 128 rows
+    static constexpr int TILE = (HD / 64) * CHUNK;     // 128 rows x HD
+    static constexpr int Q_OFF = 0;
+    static constexpr int K_OFF = 2 * TILE;
+    static constexpr int V_OFF = K_OFF + KV_STAGES * TILE;
+    static constexpr int BAR_OFF = V_OFF + KV_STAGES * TILE;
+    static constexpr int BYTES = BAR_OFF + 256 + 1024;
+};
+
+// Keep bits of 128 consecutive elements starting at global index idx0.
+template <int MODE, int R>
+__device__ __forceinline__ void keep_bits(const AttnParams& p, uint64_t idx0, uint32_t (&kw)[4]) {
+    if constexpr (MODE == MASK_BITS) {
+        if (p.bits_aligned) {  // SQ % 128 == 0: one 16-byte load per row per tile
+            const uint4 v = __ldg(reinterpret_cast<const uint4*>(p.bits + (idx0 >> 3)));
+            kw[0] = v.x; kw[1] = v.y; kw[2] = v.z; kw[3] = v.w;
+        } else {  // general: byte loads + funnel shift
+            const uint64_t b0 = idx0 >> 3;
+            const uint32_t sh = static_cast<uint32_t>(idx0 & 7);
+            uint32_t by[17];
+#pragma unroll
+            for (int t = 0; t < 17; ++t) by[t] = (b0 + t < p.bits_bytes) ? p.bits[b0 + t] : 0u;
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+                const uint64_t lo = static_cast<uint64_t>(by[4 * w]) | (static_cast<uint64_t>(by[4 * w + 1]) << 8) |
+                                    (static_cast<uint64_t>(by[4 * w + 2]) << 16) |
+                                    (static_cast<uint64_t>(by[4 * w + 3]) << 24) |
+                                    (static_cast<uint64_t>(by[4 * w + 4]) << 32);
+                kw[w] = static_cast<uint32_t>(lo >> sh);
+            }
+        }
+    } else if constexpr (MODE == MASK_PHILOX) {
+        if ((idx0 & 3) == 0) {  // 32 whole Philox blocks: same code as K1
+            const uint64_t ctr = p.base_offset + (idx0 >> 2);
+            const uint32_t lo = static_cast<uint32_t>(ctr), hi = static_cast<uint32_t>(ctr >> 32);
+            if (R > 0 && lo <= 0xFFFFFFFFu - 31u) {
+#pragma unroll
+                for (int w = 0; w < 4; ++w)
+                    kw[w] = rgo_dev::keep32_nowrap<(R > 0 ? R : 1)>(lo + 8 * w, hi, p.k0, p.k1, p.thr, 0u);
+            } else {
+#pragma unroll 1
+                for (int w = 0; w < 4; ++w) {
+                    uint32_t acc = 0;
+                    for (int b = 0; b < 8; ++b) {
+                        const uint64_t c = ctr + 8 * w + b;
+                        const uint4 o = rgo_dev::philox_rt(static_cast<uint32_t>(c), static_cast<uint32_t>(c >> 32),
+                                                           0u, 0u, p.k0, p.k1, p.rounds);
+                        acc |= (static_cast<uint32_t>(o.x < p.thr) | (static_cast<uint32_t>(o.y < p.thr) << 1) |
+                                (static_cast<uint32_t>(o.z < p.thr) << 2) | (static_cast<uint32_t>(o.w < p.thr) << 3))
+                               << (4 * b);
+                    }
+                    kw[w] = acc;
+                }
+            }
+        } else {  // misaligned row start (SQ % 4 != 0): per-element blocks
+#pragma unroll 1
+            for (int w = 0; w < 4; ++w) {
+                uint32_t acc = 0;
+                for (int c = 0; c < 32; ++c) {
+                    const uint64_t idx = idx0 + 32 * w + c;
+                    const uint64_t ctr = p.base_offset + (idx >> 2);
+                    const uint4 o = rgo_dev::philox_rt(static_cast<uint32_t>(ctr), static_cast<uint32_t>(ctr >> 32),
+                                                       0u, 0u, p.k0, p.k1, p.rounds);
+                    const uint32_t lane = static_cast<uint32_t>(idx & 3);
+                    const uint32_t wd = lane == 0 ? o.x : lane == 1 ? o.y : lane == 2 ? o.z : o.w;
+                    acc |= static_cast<uint32_t>(wd < p.thr) << c;
+                }
+                kw[w] = acc;
+            }
+        }
+    } else {
+        kw[0] = kw[1] = kw[2] = kw[3] = 0xFFFFFFFFu;
+    }
+}
+
+template <int HD, int MODE, int R>
+__global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ,
+                                                              const __grid_constant__ CUtensorMap tmK,
+                                                              const __grid_constant__ CUtensorMap tmV,
+                                                              const AttnParams p) {
+    using SM = Smem<HD>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t{1023});
+    uint8_t* sQ = smem + SM::Q_OFF;
+    uint8_t* sK = smem + SM::K_OFF;
+    uint8_t* sV = smem + SM::V_OFF;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::BAR_OFF);
+    uint64_t* q_full = bars;
+    uint64_t* k_full = bars + 1;
+    uint64_t* k_empty = k_full + KV_STAGES;
+    uint64_t* v_full = k_empty + KV_STAGES;
+    uint64_t* v_empty = v_full + KV_STAGES;
+    uint64_t* s_full = v_empty + KV_STAGES;  // [2]
+    uint64_t* p_full = s_full + 2;           // [2]
+    uint64_t* o_done = p_full + 2;           // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
+
+    const uint32_t warp = warp_id(), lane = lane_id();
+    const int pair = blockIdx.x % p.n_pairs;
+    const int bh = blockIdx.x / p.n_pairs;
+    const int hh = bh % p.H, bb = bh / p.H;
+    const int q0 = pair * 2 * BQ;
+    const int n_kv = (p.S + BKV - 1) / BKV;
+
+    if (warp == 0 && lane == 0) {
+        mbar_init(smem_u32(q_full), 1);
+        for (int s = 0; s < KV_STAGES; ++s) {
+            mbar_init(smem_u32(&k_full[s]), 1);
+            mbar_init(smem_u32(&k_empty[s]), 1);
+            mbar_init(smem_u32(&v_full[s]), 1);
+            mbar_init(smem_u32(&v_empty[s]), 1);
+        }
+        for (int w = 0; w < 2; ++w) {
+            mbar_init(smem_u32(&s_full[w]), 1);
+            mbar_init(smem_u32(&p_full[w]), 4);
+            mbar_init(smem_u32(&o_done[w]), 1);
+        }
+        fence_mbar_init();
+        tma_prefetch_desc(&tmQ);
+        tma_prefetch_desc(&tmK);
+        tma_prefetch_desc(&tmV);
+    }
+    if (warp == 1) tmem_alloc<TMEM_COLS>(smem_u32(tmem_slot));
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    constexpr int NCH = HD / 64;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ------------------------------------------------ TMA
+            const uint32_t qb = smem_u32(q_full);
+            mbar_arrive_expect_tx(qb, 2 * SM::TILE);
+            for (int w = 0; w < 2; ++w)
+                for (int c = 0; c < NCH; ++c)
+                    tma_load_4d(smem_u32(sQ + w * SM::TILE + c * SM::CHUNK), &tmQ, qb, c * 64, q0 + w * BQ, hh, bb);
+            int ks = 0, vs = 0;
+            uint32_t kph = 0, vph = 0;
+            for (int j = 0; j < n_kv; ++j) {
+                mbar_wait(smem_u32(&k_empty[ks]), kph ^ 1);
+                const uint32_t kb = smem_u32(&k_full[ks]);
+                mbar_arrive_expect_tx(kb, SM::TILE);
+                for (int c = 0; c < NCH; ++c)
+                    tma_load_4d(smem_u32(sK + ks * SM::TILE + c * SM::CHUNK), &tmK, kb, c * 64, j * BKV, hh, bb);
+                if (++ks == KV_STAGES) { ks = 0; kph ^= 1; }
+                mbar_wait(smem_u32(&v_empty[vs]), vph ^ 1);
+                const uint32_t vb = smem_u32(&v_full[vs]);
+                mbar_arrive_expect_tx(vb, SM::TILE);
+                for (int c = 0; c < NCH; ++c)
+                    tma_load_4d(smem_u32(sV + vs * SM::TILE + c * SM::CHUNK), &tmV, vb, c * 64, j * BKV, hh, bb);
+                if (++vs == KV_STAGES) { vs = 0; vph ^= 1; }
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        if (lane == 0) {  // ------------------------------------------------ MMA
+            constexpr uint32_t IDESC_S = idesc_make(1, 1, BQ, BKV, 0, 0);
+            constexpr uint32_t IDESC_O = idesc_make(1, 1, BQ, HD, 0, 1);  // V is MN-major
+            auto issue_s = [&](int w, int ks) {
+#pragma unroll
+                for (int kk = 0; kk < HD / 16; ++kk) {
+                    const uint32_t off = (kk >> 2) * SM::CHUNK + (kk & 3) * 32;
+                    const uint64_t a = desc_kmajor_sw128(smem_u32(sQ + w * SM::TILE + off));
+                    const uint64_t b = desc_kmajor_sw128(smem_u32(sK + ks * SM::TILE + off));
+                    mma_f16_ss(tmem + w * 128, a, b, IDESC_S, kk > 0);
+                }
+            };
+            auto issue_o = [&](int w, int vs, bool acc) {
+#pragma unroll
+                for (int kk = 0; kk < BKV / 16; ++kk) {
+                    // V: MN-major SW128, 8-key groups at 1024 B (SBO), 64-dH chunks at CHUNK (LBO)
+                    const uint64_t b = desc_sw128(smem_u32(sV + vs * SM::TILE + kk * 2048), SM::CHUNK, 1024);
+                    mma_f16_ts(tmem + 256 + w * 128, tmem + w * 128 + kk * 8, b, IDESC_O, (acc || kk > 0) ? 1u : 0u);
+                }
+            };
+            mbar_wait(smem_u32(q_full), 0);
+            int ks = 0, vs = 0;
+            uint32_t kph = 0, vph = 0;
+            mbar_wait(smem_u32(&k_full[ks]), kph);
+            tc_fence_after();
+            issue_s(0, ks);
+            tc_commit(smem_u32(&s_full[0]));
+            issue_s(1, ks);
+            tc_commit(smem_u32(&s_full[1]));
+            tc_commit(smem_u32(&k_empty[ks]));
+            if (++ks == KV_STAGES) { ks = 0; kph ^= 1; }
+            for (int j = 0; j < n_kv; ++j) {
+                const bool has_next = j + 1 < n_kv;
+                mbar_wait(smem_u32(&v_full[vs]), vph);
+                if (has_next) mbar_wait(smem_u32(&k_full[ks]), kph);
+                tc_fence_after();
+                for (int w = 0; w < 2; ++w) {
+                    mbar_wait(smem_u32(&p_full[w]), j & 1);
+                    tc_fence_after();
+                    issue_o(w, vs, j > 0);
+                    if (has_next) {
+                        issue_s(w, ks);
+                        tc_commit(smem_u32(&s_full[w]));
+                    }
+                }
+                tc_commit(smem_u32(&v_empty[vs]));
+                if (++vs == KV_STAGES) { vs = 0; vph ^= 1; }
+                if (has_next) {
+                    tc_commit(smem_u32(&k_empty[ks]));
+                    if (++ks == KV_STAGES) { ks = 0; kph ^= 1; }
+                }
+            }
+            tc_commit(smem_u32(&o_done[0]));
+            tc_commit(smem_u32(&o_done[1]));
+        }
+        __syncwarp();
+    } else {  // -------------------------------------------------------- softmax
+        const int w = (warp - 2) >> 2;
+        const uint32_t q = warp & 3;
+        const int row = q * 32 + lane;
+        const int i = q0 + w * BQ + row;  // query index within the slice
+        const bool row_valid = i < p.S;
+        const uint32_t lane_base = (q * 32) << 16;
+        const uint32_t tS = tmem + lane_base + w * 128;
+        const uint32_t tO = tmem + lane_base + 256 + w * 128;
+        const uint64_t slice = static_cast<uint64_t>(bb) * p.H + hh;
+        const uint64_t row_base = (slice * p.S + static_cast<uint64_t>(row_valid ? i : 0)) * p.S;
+        float m = -INFINITY, l = 0.0f;
+        for (int j = 0; j < n_kv; ++j) {
+            const int j0 = j * BKV;
+            uint32_t kw[4];
+            if (row_valid)
+                keep_bits<MODE, R>(p, row_base + j0, kw);
+            else
+                kw[0] = kw[1] = kw[2] = kw[3] = 0;
+            mbar_wait(smem_u32(&s_full[w]), j & 1);
+            tc_fence_after();
+            uint32_t s[4][32];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, s[c]);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int c = 0; c < 4; ++c) reg_fence(s[c]);
+            const int valid = p.S - j0;  // columns >= valid are padding
+            float tmax = -INFINITY;
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+#pragma unroll
+                for (int e = 0; e < 32; ++e) {
+                    float t = __uint_as_float(s[c][e]) * p.scale_log2;
+                    if (c * 32 + e >= valid) t = -INFINITY;
+                    s[c][e] = __float_as_uint(t);
+                    tmax = fmaxf(tmax, t);
+                }
+            const float m_new = fmaxf(m, tmax);
+            const bool need = m_new > m + RESCALE_THRESHOLD;
+            if (__any_sync(0xffffffffu, need)) {
+                const float alpha = exp2f(m - m_new);  // 0 on the first tile
+                if (j > 0) {
+#pragma unroll 1
+                    for (int c = 0; c < HD / 32; ++c) {
+                        uint32_t o[32];
+                        tmem_ld32(tO + c * 32, o);
+                        tmem_ld_wait_regs(o);
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+                        tmem_st32(tO + c * 32, o);
+                    }
+                }
+                l *= alpha;
+                m = m_new;
+            }
+            float rs = 0.0f;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {  // P columns [64h, 64h+64) -> TMEM cols [32h, 32h+32)
+                uint32_t pk[32];
+#pragma unroll
+                for (int cc = 0; cc < 2; ++cc) {
+                    const int c = 2 * h + cc;
+#pragma unroll
+                    for (int e = 0; e < 32; e += 2) {
+                        float p0 = exp2f(__uint_as_float(s[c][e]) - m);
+                        float p1 = exp2f(__uint_as_float(s[c][e + 1]) - m);
+                        rs += p0 + p1;
+                        if (!((kw[c] >> e) & 1u)) p0 = 0.0f;
+                        if (!((kw[c] >> (e + 1)) & 1u)) p1 = 0.0f;
+                        __nv_bfloat162 hv = __floats2bfloat162_rn(p0, p1);
+                        pk[cc * 16 + (e >> 1)] = *reinterpret_cast<uint32_t*>(&hv);
+                    }
+                }
+                tmem_st32(tS + 32 * h, pk);
+            }
+            l += rs;
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&p_full[w]));
+        }
+        // ---------------- epilogue: O / (l * keep_prob) -> bf16 rows
+        mbar_wait(smem_u32(&o_done[w]), 0);
+        tc_fence_after();
+        const float inv = 1.0f / (l * p.keep_prob);
+        __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(p.O) + bb * p.o_sb + hh * p.o_sh +
+                              static_cast<long long>(row_valid ? i : 0) * p.o_ss;
+#pragma unroll 1
+        for (int c = 0; c < HD / 32; ++c) {
+            uint32_t o[32];
+            tmem_ld32(tO + c * 32, o);
+            tmem_ld_wait_regs(o);
+            uint32_t packed[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+                __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(o[2 * e]) * inv, __uint_as_float(o[2 * e + 1]) * inv);
+                packed[e] = *reinterpret_cast<uint32_t*>(&h);
+            }
+            if (row_valid) {
+                uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+                for (int v = 0; v < 4; ++v)
+                    dst[v] = make_uint4(packed[4 * v], packed[4 * v + 1], packed[4 * v + 2], packed[4 * v + 3]);
+            }
+        }
+        if (p.lse && row_valid) p.lse[slice * p.S + i] = (m + __log2f(l)) * 0.6931471805599453f;
+    }
+    __syncthreads();
+    if (warp == 1) tmem_dealloc<TMEM_COLS>(tmem);
+}
+
+template <int HD, int MODE, int R>
+static cudaError_t launch_t(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v, const AttnParams& p,
+                            cudaStream_t s) {
+    auto kern = attn_fwd_kernel<HD, MODE, R>;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<HD>::BYTES);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    const unsigned grid = static_cast<unsigned>(p.B) * p.H * p.n_pairs;
+    kern<<<grid, THREADS, Smem<HD>::BYTES, s>>>(q, k, v, p);
+    return cudaGetLastError();
+}
+
+}  // namespace rgo_attn
+
+namespace rgo {
+
+static bool tmap_qkv(CUtensorMap* m, const AttnTensor& t, int B, int H, int S, int HD) {
+    const uint64_t dims[4] = {static_cast<uint64_t>(HD), static_cast<uint64_t>(S), static_cast<uint64_t>(H),
+                              static_cast<uint64_t>(B)};
+    const uint64_t strides[3] = {static_cast<uint64_t>(t.ss) * 2, static_cast<uint64_t>(t.sh) * 2,
+                                 static_cast<uint64_t>(t.sb) * 2};
+    const uint32_t box[4] = {64, 128, 1, 1};
+    return make_tmap(m, t.ptr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+cudaError_t launch_attn_fwd(const AttnJob& j, cudaStream_t s) {
+    using namespace rgo_attn;
+    CUtensorMap tq, tk, tv;
+    if (!tmap_qkv(&tq, j.q, j.B, j.H, j.S, j.HD) || !tmap_qkv(&tk, j.k, j.B, j.H, j.S, j.HD) ||
+        !tmap_qkv(&tv, j.v, j.B, j.H, j.S, j.HD))
+        return cudaErrorInvalidValue;
+    AttnParams p{};
+    p.B = j.B; p.H = j.H; p.S = j.S;
+    p.n_pairs = (j.S + 2 * BQ - 1) / (2 * BQ);
+    p.scale_log2 = j.scale * 1.4426950408889634f;
+    p.keep_prob = j.mode == MASK_NONE ? 1.0f : j.keep_prob;
+    p.bits = j.bits;
+    p.bits_bytes = j.bits_bytes;
+    p.bits_aligned = (j.S % 128) == 0 && (reinterpret_cast<uintptr_t>(j.bits) & 15) == 0;
+    p.k0 = static_cast<uint32_t>(j.seed);
+    p.k1 = static_cast<uint32_t>(j.seed >> 32);
+    p.base_offset = j.base_offset;
+    p.thr = static_cast<uint32_t>(j.threshold);
+    p.rounds = j.rounds;
+    p.O = j.o.ptr;
+    p.o_sb = j.o.sb; p.o_sh = j.o.sh; p.o_ss = j.o.ss;
+    p.lse = j.lse;
+    int mode = j.mode;
+    // keep-all (threshold 2^32) or keep_prob 1: every bit is 1 -> plain path, scale 1/p
+    if (mode == MASK_PHILOX && j.threshold >= (uint64_t{1} << 32)) mode = MASK_NONE;
+#define RGO_A(HDV, MODEV, RV) \
+    if (j.HD == HDV && mode == MODEV) return launch_t<HDV, MODEV, RV>(tq, tk, tv, p, s);
+    RGO_A(128, MASK_NONE, 0)
+    RGO_A(64, MASK_NONE, 0)
+    RGO_A(128, MASK_BITS, 0)
+    RGO_A(64, MASK_BITS, 0)
+    if (mode == MASK_PHILOX) {
+        if (j.rounds == 10) {
+            RGO_A(128, MASK_PHILOX, 10)
+            RGO_A(64, MASK_PHILOX, 10)
+        } else if (j.rounds == 7) {
+            RGO_A(128, MASK_PHILOX, 7)
+            RGO_A(64, MASK_PHILOX, 7)
+        } else {
+            RGO_A(128, MASK_PHILOX, 0)
+            RGO_A(64, MASK_PHILOX, 0)
+        }
+    }
+#undef RGO_A
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace rgo

@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "rgo/capi.h"
+#include "attn.h"
 #include "gemm.h"
 #include "rgo_internal.h"
 
@@ -304,6 +305,57 @@ int rgo_gemm_with_rng(const rgo_gemm_desc* g, const void* d_a, const void* d_b, 
     j.rng = &q;
     cudaError_t ce = rgo::launch_gemm(j, static_cast<cudaStream_t>(stream));
     return ce == cudaSuccess ? RGO_OK : cuda_fail(ce, "rgo_gemm_with_rng");
+}
+
+int rgo_attn_fwd(const rgo_attn_desc* a, const rgo_tensor4* q, const rgo_tensor4* k,
+                 const rgo_tensor4* v, const uint8_t* d_bits, uint64_t bits_bytes,
+                 const rgo_tensor4* o, float* d_lse, rgo_stream_t stream) {
+    if (!a || !q || !k || !v || !o) return fail(RGO_EINVAL, "rgo_attn_fwd: null argument");
+    if (a->batch < 1 || a->heads < 1 || a->seq < 1 || a->head_dim < 1)
+        return fail(RGO_EINVAL, "attention dims must be >= 1");
+    if (a->head_dim != 64 && a->head_dim != 128)
+        return fail(RGO_EINVAL, "rgo_attn_fwd: head_dim must be 64 or 128 (pad smaller heads)");
+    if (a->mask_source < RGO_MASK_NONE || a->mask_source > RGO_MASK_PHILOX)
+        return fail(RGO_EINVAL, "rgo_attn_fwd: bad mask source");
+    const bool drop = a->mask_source != RGO_MASK_NONE;
+    if (drop && !(a->keep_prob > 0.0 && a->keep_prob <= 1.0))  // ref_attention.hpp:117-118
+        return fail(RGO_EINVAL, "attention_dropout: p must be in (0,1]");
+    const uint64_t n = static_cast<uint64_t>(a->batch) * a->heads * a->seq * static_cast<uint64_t>(a->seq);
+    if (a->mask_source == RGO_MASK_BITS && (!d_bits || bits_bytes < (n + 7) / 8))
+        return fail(RGO_EINVAL, "attention_dropout_decoupled: mask needs %llu bytes",
+                    static_cast<unsigned long long>((n + 7) / 8));
+    if (a->mask_source == RGO_MASK_PHILOX && (a->rounds < 1 || a->rounds > 16))
+        return fail(RGO_EINVAL, "attention_dropout_fused: rounds must be in [1,16]");
+    const rgo_tensor4* ts[4] = {q, k, v, o};
+    for (const rgo_tensor4* t : ts) {
+        if (!t->ptr || (reinterpret_cast<uintptr_t>(t->ptr) & 15) || ((t->stride_b | t->stride_h | t->stride_s) * 2) % 16)
+            return fail(RGO_EINVAL, "rgo_attn_fwd: tensors need 16-byte aligned base and strides");
+    }
+    if (int e = require_device()) return e;
+    rgo::AttnJob j{};
+    j.B = static_cast<int>(a->batch);
+    j.H = static_cast<int>(a->heads);
+    j.S = static_cast<int>(a->seq);
+    j.HD = static_cast<int>(a->head_dim);
+    j.scale = a->scale > 0 ? a->scale : 1.0f / std::sqrt(static_cast<float>(a->head_dim));
+    j.q = {q->ptr, q->stride_b, q->stride_h, q->stride_s};
+    j.k = {k->ptr, k->stride_b, k->stride_h, k->stride_s};
+    j.v = {v->ptr, v->stride_b, v->stride_h, v->stride_s};
+    j.o = {const_cast<void*>(o->ptr), o->stride_b, o->stride_h, o->stride_s};
+    j.lse = d_lse;
+    j.mode = a->mask_source;
+    float kp = 1.0f;
+    uint64_t thr = uint64_t{1} << 32;
+    rgo_keep_threshold(drop ? a->keep_prob : 1.0, &thr, &kp);
+    j.keep_prob = kp;
+    j.threshold = thr;
+    j.bits = d_bits;
+    j.bits_bytes = bits_bytes;
+    j.seed = a->seed;
+    j.base_offset = a->base_offset;
+    j.rounds = static_cast<int>(a->rounds);
+    cudaError_t ce = rgo::launch_attn_fwd(j, static_cast<cudaStream_t>(stream));
+    return ce == cudaSuccess ? RGO_OK : cuda_fail(ce, "rgo_attn_fwd");
 }
 
 }  // extern "C"

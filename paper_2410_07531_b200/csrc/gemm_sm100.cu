@@ -216,7 +216,8 @@ __global__ void __launch_bounds__(CORE_THREADS + 32 * RNG_WARPS, 1)
                     uint32_t g[32], u[32];
                     tmem_ld32(tbase + c * 32, g);
                     tmem_ld32(tbase + 128 + c * 32, u);
-                    tmem_ld_wait();
+                    tmem_ld_wait_regs(g);
+                    reg_fence(u);
                     float v[32];
 #pragma unroll
                     for (int i = 0; i < 32; ++i)
@@ -230,7 +231,7 @@ __global__ void __launch_bounds__(CORE_THREADS + 32 * RNG_WARPS, 1)
                 for (int c = 0; c < BN / 32; ++c) {
                     uint32_t r[32];
                     tmem_ld32(tbase + c * 32, r);
-                    tmem_ld_wait();
+                    tmem_ld_wait_regs(r);
                     float v[32];
 #pragma unroll
                     for (int i = 0; i < 32; ++i) {

@@ -39,7 +39,10 @@ def test_fp8_gemm(rgo, cuda, m, n, k):
     ref = (a.float() @ b.float().T) / 64
     assert rel(c, ref) < 5e-3  # exact products, fp32 accumulate, bf16 output
     c8 = rgo.gemm(a, b, alpha=1.0 / 64, out_scale=0.5, out_dtype=torch.float8_e4m3fn)
-    assert rel(c8.float(), ref * 0.5) < 2e-2
+    # e4m3 output rounding (3 mantissa bits) dominates: compare with the
+    # fp8-rounded reference, then bound the total error by the format's RMS
+    assert rel(c8.float(), (ref * 0.5).to(torch.float8_e4m3fn).float()) < 2e-2
+    assert rel(c8.float(), ref * 0.5) < 4e-2
 
 
 def test_swiglu_epilogue(rgo, cuda):
@@ -60,7 +63,7 @@ def test_gelu_epilogue_fp8_out(rgo, cuda):
     b = make((512, 512), torch.float32, 9, 2.0).to(torch.float8_e4m3fn)
     c = rgo.gemm(a, b, epilogue="gelu", alpha=1 / 32, out_scale=4.0, out_dtype=torch.float8_e4m3fn)
     ref = torch.nn.functional.gelu((a.float() @ b.float().T) / 32, approximate="tanh") * 4.0
-    assert rel(c.float(), ref) < 2e-2
+    assert rel(c.float(), ref.to(torch.float8_e4m3fn).float()) < 2e-2
 
 
 def test_gemm_with_rng_mask_and_output(rgo, cuda):
