@@ -186,6 +186,59 @@ int rgo_attn_fwd(const rgo_attn_desc* a, const rgo_tensor4* q, const rgo_tensor4
                  const rgo_tensor4* v, const uint8_t* d_bits, uint64_t bits_bytes,
                  const rgo_tensor4* o, float* d_lse, rgo_stream_t stream);
 
+/* ----------------------------------------------------------------- block --
+ * Transformer-block step (the paper's timeline, schedule.hpp:111-136): the
+ * four GEMMs between consecutive attention layers (Proj, FFN1, FFN2 of block
+ * L-1 and QKV of block L, all FP8) followed by the attention of block L.
+ * Modes: SERIAL_FUSED = baseline (attention regenerates Philox inline);
+ * STREAMS = mechanism A (K1 on a low-priority stream, capped grid, event join);
+ * IN_GEMM = mechanism B (RNG warps co-resident in the GEMM CTAs + tail drain).
+ * The caller owns every buffer; the handle owns streams, events and the
+ * captured CUDA graph. */
+typedef enum rgo_overlap_mode {
+    RGO_OVERLAP_SERIAL_FUSED = 0,
+    RGO_OVERLAP_STREAMS = 1,
+    RGO_OVERLAP_IN_GEMM = 2
+} rgo_overlap_mode;
+
+typedef struct rgo_block_desc {
+    uint32_t batch, seq, heads, head_dim, ffn;
+    int32_t gated;          /* 1: SwiGLU FFN1 with 2*ffn outputs; 0: GELU */
+    double keep_prob;       /* (0,1) */
+    uint32_t rounds;        /* Philox rounds */
+    uint32_t use_graph;     /* capture the step into a CUDA graph */
+    uint64_t seed, base_offset;  /* mask layout of batch*heads slices */
+    float a_qkv, a_proj, a_ffn1, a_ffn2;  /* FP8 dequant scales */
+    float s_attn, s_proj, s_ffn1, s_ffn2; /* output quantisation scales */
+    rgo_launch rng_launch;  /* STREAMS: mask-kernel launch shape */
+} rgo_block_desc;
+
+typedef struct rgo_block_buffers {
+    void* x;        /* e4m3 [M, d], M = batch*seq, d = heads*head_dim */
+    void* wqkv;     /* e4m3 [3d, d] */
+    void* wo;       /* e4m3 [d, d] */
+    void* w1;       /* e4m3 [n1, d], n1 = 2*ffn (gated) or ffn */
+    void* w2;       /* e4m3 [d, ffn] */
+    void* qkv;      /* bf16 [M, 3d] */
+    void* attn_o;   /* bf16 [M, d] */
+    void* attn_o8;  /* e4m3 [M, d] */
+    void* y1;       /* e4m3 [M, d] */
+    void* h;        /* e4m3 [M, ffn] */
+    uint8_t* mask;  /* B*nH*S^2/8 bytes */
+    uint64_t mask_bytes;
+    unsigned long long* counter; /* IN_GEMM work-queue counter */
+    float* lse;     /* optional [B*nH*S] */
+} rgo_block_buffers;
+
+typedef struct rgo_block rgo_block;
+
+int rgo_block_create(const rgo_block_desc* d, const rgo_block_buffers* b, int32_t mode,
+                     rgo_block** out);
+/* Enqueue one step ordered after prior work on `stream`; *launches (optional)
+ * = number of kernels the step launches. */
+int rgo_block_step(rgo_block* blk, rgo_stream_t stream, int32_t* launches);
+int rgo_block_destroy(rgo_block* blk);
+
 #ifdef __cplusplus
 }
 #endif

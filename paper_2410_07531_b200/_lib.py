@@ -70,6 +70,23 @@ class attn_desc(C.Structure):
     ]
 
 
+class block_desc(C.Structure):
+    _fields_ = [
+        ("batch", C.c_uint32), ("seq", C.c_uint32), ("heads", C.c_uint32), ("head_dim", C.c_uint32),
+        ("ffn", C.c_uint32), ("gated", C.c_int32), ("keep_prob", C.c_double), ("rounds", C.c_uint32),
+        ("use_graph", C.c_uint32), ("seed", C.c_uint64), ("base_offset", C.c_uint64),
+        ("a_qkv", C.c_float), ("a_proj", C.c_float), ("a_ffn1", C.c_float), ("a_ffn2", C.c_float),
+        ("s_attn", C.c_float), ("s_proj", C.c_float), ("s_ffn1", C.c_float), ("s_ffn2", C.c_float),
+        ("rng_launch", launch),
+    ]
+
+
+class block_buffers(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("x", "wqkv", "wo", "w1", "w2", "qkv", "attn_o", "attn_o8", "y1", "h",
+                                          "mask")] + [("mask_bytes", C.c_uint64), ("counter", C.c_void_p),
+                                                      ("lse", C.c_void_p)]
+
+
 # name -> (restype, argtypes).  Every symbol include/rgo/capi.h declares.
 SIGNATURES = {
     "rgo_last_error": (C.c_char_p, []),
@@ -105,6 +122,9 @@ SIGNATURES = {
         [C.POINTER(attn_desc), C.POINTER(tensor4), C.POINTER(tensor4), C.POINTER(tensor4), C.c_void_p,
          C.c_uint64, C.POINTER(tensor4), C.c_void_p, C.c_void_p],
     ),
+    "rgo_block_create": (C.c_int, [C.POINTER(block_desc), C.POINTER(block_buffers), C.c_int32, C.c_void_p]),
+    "rgo_block_step": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "rgo_block_destroy": (C.c_int, [C.c_void_p]),
     "rgo_uniform_fill": (
         C.c_int,
         [C.c_uint64, C.c_uint32, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p],

@@ -1,0 +1,109 @@
+"""Transformer-block step (QKV/Proj/FFN GEMMs + attention with dropout) on
+the B200 runtime (csrc/block.cu) through the C ABI (rgo_block_*).
+
+Synthetic, random-init weights and activations of the named shape (no
+checkpoints): values from the reference's Philox generator
+(random_attention_input's counter layout, streams 4+), quantised per tensor
+to E4M3.  Scales keep every intermediate O(1) so nothing saturates.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+from . import _lib
+from .gemm import WorkloadConfig
+from .mask import KeepThreshold
+
+MODES = {"serial_fused": 0, "streams": 1, "in_gemm": 2}
+
+
+def _uniform(n, stream_id, seed, device):
+    import torch
+    t = torch.empty(n, dtype=torch.float32, device=device)
+    _lib.check(_lib.lib().rgo_uniform_fill(seed, stream_id, n, None, t.data_ptr(),
+                                           torch.cuda.current_stream().cuda_stream))
+    return t
+
+
+class Block:
+    """Owns the device buffers of one block replica and the C-ABI handle."""
+
+    def __init__(self, cfg: WorkloadConfig, mode: str = "streams", seed: int = 42, base_offset: int = 0,
+                 rng_launch=(0, 0, 0), use_graph: bool = True, device="cuda", weights=None):
+        import torch
+        self.cfg, self.mode = cfg, mode
+        B, S, H, D = cfg.batch, cfg.seq, cfg.heads, cfg.head_dim
+        d, F = H * D, cfg.ffn()
+        n1 = 2 * F if cfg.gated else F
+        M = B * S
+        self.M, self.d, self.F, self.n1 = M, d, F, n1
+        f8, bf = torch.float8_e4m3fn, torch.bfloat16
+        dev = torch.device(device)
+        if weights is None:
+            weights = make_weights(cfg, seed, dev)
+        self.weights = weights
+        self.x = _uniform(M * d, 8, seed, dev).view(M, d).to(f8)
+        self.qkv = torch.empty(M, 3 * d, dtype=bf, device=dev)
+        self.attn_o = (_uniform(M * d, 9, seed, dev).view(M, d) * 0.1).to(bf)
+        self.attn_o8 = torch.empty(M, d, dtype=f8, device=dev)
+        self.y1 = torch.empty(M, d, dtype=f8, device=dev)
+        self.h = torch.empty(M, F, dtype=f8, device=dev)
+        elems = B * H * S * S
+        self.mask = torch.zeros(elems // 8, dtype=torch.uint8, device=dev)
+        self.counter = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.lse = None
+        ku = 3.0  # E[(U(-1,1))^2] = 1/3 -> alpha = 3/sqrt(K) gives unit-variance outputs
+        desc = _lib.block_desc()
+        desc.batch, desc.seq, desc.heads, desc.head_dim, desc.ffn = B, S, H, D, F
+        desc.gated = 1 if cfg.gated else 0
+        desc.keep_prob = cfg.keep_prob
+        desc.rounds = cfg.philox_rounds
+        desc.use_graph = 1 if use_graph else 0
+        desc.seed, desc.base_offset = seed, base_offset
+        desc.a_qkv, desc.a_proj = ku / math.sqrt(d), ku / math.sqrt(d)
+        desc.a_ffn1, desc.a_ffn2 = ku / math.sqrt(d), ku / math.sqrt(F)
+        desc.s_attn, desc.s_proj, desc.s_ffn1, desc.s_ffn2 = 8.0, 1.0, 2.0, 1.0
+        desc.rng_launch = _lib.launch(*rng_launch, 0)
+        self.desc = desc
+        w = weights
+        bufs = _lib.block_buffers(self.x.data_ptr(), w["wqkv"].data_ptr(), w["wo"].data_ptr(), w["w1"].data_ptr(),
+                                  w["w2"].data_ptr(), self.qkv.data_ptr(), self.attn_o.data_ptr(),
+                                  self.attn_o8.data_ptr(), self.y1.data_ptr(), self.h.data_ptr(),
+                                  self.mask.data_ptr(), self.mask.numel(), self.counter.data_ptr(), None)
+        self._bufs = bufs
+        handle = C.c_void_p()
+        torch.cuda.synchronize()
+        _lib.check(_lib.lib().rgo_block_create(desc, bufs, MODES[mode], C.byref(handle)))
+        self.handle = handle
+
+    def step(self, stream=None) -> int:
+        import torch
+        s = (stream or torch.cuda.current_stream()).cuda_stream
+        n = C.c_int32()
+        _lib.check(_lib.lib().rgo_block_step(self.handle, s, C.byref(n)))
+        return n.value
+
+    def close(self):
+        if getattr(self, "handle", None):
+            _lib.lib().rgo_block_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def make_weights(cfg: WorkloadConfig, seed: int, device):
+    import torch
+    d, F = cfg.heads * cfg.head_dim, cfg.ffn()
+    n1 = 2 * F if cfg.gated else F
+    f8 = torch.float8_e4m3fn
+    return {
+        "wqkv": _uniform(3 * d * d, 4, seed, device).view(3 * d, d).to(f8),
+        "wo": _uniform(d * d, 5, seed, device).view(d, d).to(f8),
+        "w1": _uniform(n1 * d, 6, seed, device).view(n1, d).to(f8),
+        "w2": _uniform(d * F, 7, seed, device).view(d, F).to(f8),
+    }

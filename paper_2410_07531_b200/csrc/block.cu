@@ -1,0 +1,253 @@
+// block.cu -- transformer-block runtime: the paper's timeline on silicon.
+//
+// One block = QKV GEMM -> attention -> Proj GEMM -> FFN1 GEMM -> FFN2 GEMM
+// (proj/include/rgo/workload.hpp:3-6, :44-52; LayerNorm/residual omitted as
+// in the reference).  A "step" is the steady-state rotation
+//     [Proj, FFN1, FFN2 of block L-1, QKV of block L]  ->  attention of block L
+// so the four GEMMs between consecutive attention layers form the window the
+// RNG hides under (schedule.hpp:111-136):
+//   SERIAL_FUSED  baseline: GEMMs, then attention with Philox inline (K6)
+//   STREAMS       mechanism A: mask kernel (K1) on a low-priority stream with a
+//                 grid capped to co-reside with the GEMM CTAs; GEMMs on a
+//                 high-priority stream; attention (K5) waits on an event
+//   IN_GEMM       mechanism B: the GEMMs carry co-resident RNG warps draining
+//                 the mask queue (K4); a tail drain finishes any remainder
+// Each step is captured once into a CUDA graph and replayed.
+#include <cuda_bf16.h>
+#include <cuda_fp8.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <new>
+
+#include "attn.h"
+#include "block.h"
+#include "gemm.h"
+#include "rgo_internal.h"
+
+namespace rgo_dev {
+
+// bf16 -> e4m3 (saturating) with a scale; 16 elements per thread.
+__global__ void quant_e4m3_kernel(const __nv_bfloat16* __restrict__ in, uint8_t* __restrict__ out, uint64_t n,
+                                  float scale) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x * 16;
+    for (uint64_t i = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 16; i < n; i += stride) {
+        if (i + 16 <= n) {
+            const uint4 a = *reinterpret_cast<const uint4*>(in + i);
+            const uint4 b = *reinterpret_cast<const uint4*>(in + i + 8);
+            const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+            uint32_t o[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const float2 f0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[2 * k]));
+                const float2 f1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[2 * k + 1]));
+                const __nv_fp8x2_storage_t lo = __nv_cvt_float2_to_fp8x2(make_float2(f0.x * scale, f0.y * scale),
+                                                                         __NV_SATFINITE, __NV_E4M3);
+                const __nv_fp8x2_storage_t hi = __nv_cvt_float2_to_fp8x2(make_float2(f1.x * scale, f1.y * scale),
+                                                                         __NV_SATFINITE, __NV_E4M3);
+                o[k] = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
+            }
+            *reinterpret_cast<uint4*>(out + i) = make_uint4(o[0], o[1], o[2], o[3]);
+        } else {
+            for (uint64_t t = i; t < n; ++t)
+                out[t] = __nv_cvt_float_to_fp8(__bfloat162float(in[t]) * scale, __NV_SATFINITE, __NV_E4M3);
+        }
+    }
+}
+
+}  // namespace rgo_dev
+
+namespace rgo {
+
+cudaError_t launch_quant_e4m3(const void* in, void* out, uint64_t n, float scale, cudaStream_t s) {
+    const uint64_t threads = (n + 15) / 16;
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((threads + 255) / 256, 148 * 16));
+    rgo_dev::quant_e4m3_kernel<<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(in),
+                                                    static_cast<uint8_t*>(out), n, scale);
+    return cudaGetLastError();
+}
+
+struct Block {
+    BlockConfig cfg;
+    BlockBuffers buf;
+    int mode;
+    cudaStream_t s_main = nullptr, s_rng = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_rng = nullptr;  // fork/join inside a step
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr;    // ordering against the caller's stream
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    int launches_per_step = 0;
+};
+
+static GemmJob gemm(const BlockConfig& c, int M, int N, int K, const void* A, const void* B, void* C, int epi,
+                    int out, float alpha, float out_scale) {
+    GemmJob j{};
+    j.fp8 = true;
+    j.M = M; j.N = N; j.K = K;
+    j.A = A; j.lda = K; j.B = B; j.ldb = K;
+    j.C = C;
+    j.ldc = epi == rgo_gk::EPI_SWIGLU ? N / 2 : N;
+    j.epi = epi; j.out = out;
+    j.alpha = alpha; j.out_scale = out_scale;
+    j.grid = 0;
+    j.rng = nullptr;
+    (void)c;
+    return j;
+}
+
+// Enqueue one step on b.s_main (+ b.s_rng); returns #kernels launched.
+static cudaError_t enqueue_step(Block& b, int* launches) {
+    const BlockConfig& c = b.cfg;
+    const BlockBuffers& x = b.buf;
+    const int M = c.batch * c.seq, d = c.heads * c.head_dim, F = c.ffn;
+    const int n1 = c.gated ? 2 * F : F;
+    const uint64_t elems = static_cast<uint64_t>(c.batch) * c.heads * c.seq * static_cast<uint64_t>(c.seq);
+    cudaStream_t s = b.s_main;
+    int n = 0;
+    cudaError_t e;
+    RngQueue q{};
+    q.out = x.mask;
+    q.n_vec = elems / 128;
+    q.base_offset = c.base_offset;
+    q.k0 = static_cast<uint32_t>(c.seed);
+    q.k1 = static_cast<uint32_t>(c.seed >> 32);
+    q.thr = static_cast<uint32_t>(c.threshold);
+    q.rounds = c.rounds;
+    q.counter = x.counter;
+
+    if (b.mode == BLOCK_STREAMS) {  // fork: K1 on the low-priority stream
+        if ((e = cudaEventRecord(b.ev_fork, s)) != cudaSuccess) return e;
+        if ((e = cudaStreamWaitEvent(b.s_rng, b.ev_fork, 0)) != cudaSuccess) return e;
+        MaskJob mj{x.mask, elems, c.seed, c.base_offset, c.threshold, c.rounds};
+        LaunchShape ls;
+        ls.grid = c.rng_grid;
+        ls.block = c.rng_block;
+        ls.dyn_smem = c.rng_smem;
+        if ((e = launch_mask(mj, ls, b.s_rng)) != cudaSuccess) return e;
+        ++n;
+        if ((e = cudaEventRecord(b.ev_rng, b.s_rng)) != cudaSuccess) return e;
+    } else if (b.mode == BLOCK_IN_GEMM) {
+        if ((e = cudaMemsetAsync(x.counter, 0, sizeof(unsigned long long), s)) != cudaSuccess) return e;
+    }
+    const RngQueue* rq = b.mode == BLOCK_IN_GEMM ? &q : nullptr;
+    // attention output of the previous block -> e4m3
+    if ((e = launch_quant_e4m3(x.attn_o, x.attn_o8, static_cast<uint64_t>(M) * d, c.s_attn, s)) != cudaSuccess)
+        return e;
+    ++n;
+    GemmJob g;
+    g = gemm(c, M, d, d, x.attn_o8, x.wo, x.y1, rgo_gk::EPI_NONE, rgo_gk::OUT_E4M3, c.a_proj, c.s_proj);
+    g.rng = rq;
+    if ((e = launch_gemm(g, s)) != cudaSuccess) return e;
+    ++n;
+    g = gemm(c, M, n1, d, x.y1, x.w1, x.h, c.gated ? rgo_gk::EPI_SWIGLU : rgo_gk::EPI_GELU, rgo_gk::OUT_E4M3,
+             c.a_ffn1, c.s_ffn1);
+    g.rng = rq;
+    if ((e = launch_gemm(g, s)) != cudaSuccess) return e;
+    ++n;
+    g = gemm(c, M, d, F, x.h, x.w2, x.x, rgo_gk::EPI_NONE, rgo_gk::OUT_E4M3, c.a_ffn2, c.s_ffn2);
+    g.rng = rq;
+    if ((e = launch_gemm(g, s)) != cudaSuccess) return e;
+    ++n;
+    g = gemm(c, M, 3 * d, d, x.x, x.wqkv, x.qkv, rgo_gk::EPI_NONE, rgo_gk::OUT_BF16, c.a_qkv, 1.0f);
+    g.rng = rq;
+    if ((e = launch_gemm(g, s)) != cudaSuccess) return e;
+    ++n;
+    if (b.mode == BLOCK_IN_GEMM) {  // tail: whatever the GEMM-resident warps left
+        if ((e = launch_rng_queue(q, 0, 0, 0, s)) != cudaSuccess) return e;
+        ++n;
+    } else if (b.mode == BLOCK_STREAMS) {
+        if ((e = cudaStreamWaitEvent(s, b.ev_rng, 0)) != cudaSuccess) return e;
+    }
+    // attention on the QKV GEMM output (token-major [M, 3d]) -> attn_o [M, d]
+    AttnJob a{};
+    a.B = c.batch; a.H = c.heads; a.S = c.seq; a.HD = c.head_dim;
+    a.scale = 1.0f / sqrtf(static_cast<float>(c.head_dim));
+    const long long ld = 3LL * d;
+    const __nv_bfloat16* qkv = static_cast<const __nv_bfloat16*>(x.qkv);
+    a.q = {qkv, static_cast<long long>(c.seq) * ld, c.head_dim, ld};
+    a.k = {qkv + d, static_cast<long long>(c.seq) * ld, c.head_dim, ld};
+    a.v = {qkv + 2 * d, static_cast<long long>(c.seq) * ld, c.head_dim, ld};
+    a.o = {x.attn_o, static_cast<long long>(c.seq) * d, c.head_dim, d};
+    a.lse = x.lse;
+    a.mode = b.mode == BLOCK_SERIAL_FUSED ? rgo_attn::MASK_PHILOX : rgo_attn::MASK_BITS;
+    a.keep_prob = c.keep_prob;
+    a.bits = x.mask;
+    a.bits_bytes = x.mask_bytes;
+    a.seed = c.seed;
+    a.base_offset = c.base_offset;
+    a.threshold = c.threshold;
+    a.rounds = c.rounds;
+    if ((e = launch_attn_fwd(a, s)) != cudaSuccess) return e;
+    ++n;
+    *launches = n;
+    return cudaSuccess;
+}
+
+cudaError_t block_create(const BlockConfig& cfg, const BlockBuffers& buf, int mode, bool use_graph, Block** out) {
+    Block* b = new (std::nothrow) Block();
+    if (!b) return cudaErrorMemoryAllocation;
+    b->cfg = cfg;
+    b->buf = buf;
+    b->mode = mode;
+    int lo = 0, hi = 0;
+    cudaError_t e = cudaDeviceGetStreamPriorityRange(&lo, &hi);  // hi = greatest priority (numerically lowest)
+    if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&b->s_main, cudaStreamNonBlocking, hi);
+    if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&b->s_rng, cudaStreamNonBlocking, lo);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&b->ev_fork, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&b->ev_rng, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&b->ev_in, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&b->ev_out, cudaEventDisableTiming);
+    if (e == cudaSuccess && use_graph) {
+        // (kernel attributes and tensor maps are host-side calls, legal during capture;
+        // no step is executed here, so creating a block never touches its buffers)
+        e = cudaStreamBeginCapture(b->s_main, cudaStreamCaptureModeThreadLocal);
+        if (e == cudaSuccess) {
+            cudaError_t e2 = enqueue_step(*b, &b->launches_per_step);
+            e = cudaStreamEndCapture(b->s_main, &b->graph);
+            if (e2 != cudaSuccess) e = e2;
+        }
+        if (e == cudaSuccess) e = cudaGraphInstantiate(&b->exec, b->graph, 0);
+    }
+    if (e != cudaSuccess) {
+        block_destroy(b);
+        return e;
+    }
+    *out = b;
+    return cudaSuccess;
+}
+
+// Run one step ordered after `stream` (and before later work on it).
+cudaError_t block_step(Block* b, cudaStream_t stream, int* launches) {
+    cudaError_t e;
+    if ((e = cudaEventRecord(b->ev_in, stream)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(b->s_main, b->ev_in, 0)) != cudaSuccess) return e;
+    int n = 0;
+    if (b->exec) {
+        e = cudaGraphLaunch(b->exec, b->s_main);
+        n = b->launches_per_step;
+    } else {
+        e = enqueue_step(*b, &n);
+    }
+    if (e != cudaSuccess) return e;
+    if ((e = cudaEventRecord(b->ev_out, b->s_main)) != cudaSuccess) return e;
+    if (launches) *launches = n;
+    return cudaStreamWaitEvent(stream, b->ev_out, 0);
+}
+
+void block_destroy(Block* b) {
+    if (!b) return;
+    if (b->exec) cudaGraphExecDestroy(b->exec);
+    if (b->graph) cudaGraphDestroy(b->graph);
+    if (b->ev_fork) cudaEventDestroy(b->ev_fork);
+    if (b->ev_rng) cudaEventDestroy(b->ev_rng);
+    if (b->ev_in) cudaEventDestroy(b->ev_in);
+    if (b->ev_out) cudaEventDestroy(b->ev_out);
+    if (b->s_main) cudaStreamDestroy(b->s_main);
+    if (b->s_rng) cudaStreamDestroy(b->s_rng);
+    delete b;
+}
+
+}  // namespace rgo

@@ -1,0 +1,48 @@
+// block.h -- internal transformer-block runtime interface (see block.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace rgo {
+
+enum { BLOCK_SERIAL_FUSED = 0, BLOCK_STREAMS = 1, BLOCK_IN_GEMM = 2 };
+
+struct BlockConfig {
+    int batch, seq, heads, head_dim, ffn;
+    int gated;                   // SwiGLU FFN1 (2*ffn outputs) else GELU
+    float keep_prob;             // float keep probability
+    uint64_t threshold;          // KeepThreshold::threshold(), < 2^32
+    int rounds;
+    uint64_t seed, base_offset;  // mask layout (batch*heads slices)
+    // per-tensor FP8 scales: alpha = dequant of A.B, s_* = output quantisation
+    float a_qkv, a_proj, a_ffn1, a_ffn2;
+    float s_attn, s_proj, s_ffn1, s_ffn2;
+    // mechanism A launch shape of the mask kernel (0 = auto)
+    unsigned rng_grid, rng_block, rng_smem;
+};
+
+struct BlockBuffers {
+    void* x;        // e4m3 [M, d]   block input (= FFN2 output of the previous block)
+    void* wqkv;     // e4m3 [3d, d]
+    void* wo;       // e4m3 [d, d]
+    void* w1;       // e4m3 [n1, d]  (SwiGLU: per 256-row tile [128 gate | 128 up])
+    void* w2;       // e4m3 [d, ffn]
+    void* qkv;      // bf16 [M, 3d]
+    void* attn_o;   // bf16 [M, d]
+    void* attn_o8;  // e4m3 [M, d]
+    void* y1;       // e4m3 [M, d]
+    void* h;        // e4m3 [M, ffn]
+    uint8_t* mask;  // packed dropout mask, B*nH*S^2/8 bytes
+    uint64_t mask_bytes;
+    unsigned long long* counter;  // mask work-queue counter (IN_GEMM)
+    float* lse;     // optional [B*nH*S]
+};
+
+struct Block;
+cudaError_t block_create(const BlockConfig& cfg, const BlockBuffers& buf, int mode, bool use_graph, Block** out);
+cudaError_t block_step(Block* b, cudaStream_t stream, int* launches);
+void block_destroy(Block* b);
+cudaError_t launch_quant_e4m3(const void* in, void* out, uint64_t n, float scale, cudaStream_t s);
+
+}  // namespace rgo

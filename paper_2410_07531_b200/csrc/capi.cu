@@ -16,6 +16,7 @@
 
 #include "rgo/capi.h"
 #include "attn.h"
+#include "block.h"
 #include "gemm.h"
 #include "rgo_internal.h"
 
@@ -356,6 +357,63 @@ int rgo_attn_fwd(const rgo_attn_desc* a, const rgo_tensor4* q, const rgo_tensor4
     j.rounds = static_cast<int>(a->rounds);
     cudaError_t ce = rgo::launch_attn_fwd(j, static_cast<cudaStream_t>(stream));
     return ce == cudaSuccess ? RGO_OK : cuda_fail(ce, "rgo_attn_fwd");
+}
+
+struct rgo_block {
+    rgo::Block* impl;
+};
+
+int rgo_block_create(const rgo_block_desc* d, const rgo_block_buffers* b, int32_t mode, rgo_block** out) {
+    if (!d || !b || !out) return fail(RGO_EINVAL, "rgo_block_create: null argument");
+    if (mode < RGO_OVERLAP_SERIAL_FUSED || mode > RGO_OVERLAP_IN_GEMM)
+        return fail(RGO_EINVAL, "rgo_block_create: bad overlap mode");
+    if (d->head_dim != 64 && d->head_dim != 128) return fail(RGO_EINVAL, "rgo_block_create: head_dim 64/128");
+    if (!(d->keep_prob > 0.0 && d->keep_prob < 1.0)) return fail(RGO_EINVAL, "rgo_block_create: keep_prob in (0,1)");
+    if (d->rounds < 1 || d->rounds > 16) return fail(RGO_EINVAL, "rgo_block_create: rounds must be in [1,16]");
+    const uint64_t dm = static_cast<uint64_t>(d->heads) * d->head_dim;
+    if (dm % 256 || d->ffn % 128 || (static_cast<uint64_t>(d->batch) * d->seq) % 128 || d->seq % 128)
+        return fail(RGO_EINVAL, "rgo_block_create: needs d %% 256, ffn %% 128, seq %% 128 == 0");
+    if (d->gated && d->ffn % 128) return fail(RGO_EINVAL, "rgo_block_create: gated ffn %% 128");
+    const uint64_t n = static_cast<uint64_t>(d->batch) * d->heads * d->seq * static_cast<uint64_t>(d->seq);
+    if (!b->mask || b->mask_bytes < n / 8 || !b->counter || !b->x || !b->wqkv || !b->wo || !b->w1 || !b->w2 ||
+        !b->qkv || !b->attn_o || !b->attn_o8 || !b->y1 || !b->h)
+        return fail(RGO_EINVAL, "rgo_block_create: missing buffer (mask needs %llu bytes)",
+                    static_cast<unsigned long long>(n / 8));
+    if (int e = require_device()) return e;
+    rgo::BlockConfig c{};
+    c.batch = static_cast<int>(d->batch); c.seq = static_cast<int>(d->seq);
+    c.heads = static_cast<int>(d->heads); c.head_dim = static_cast<int>(d->head_dim);
+    c.ffn = static_cast<int>(d->ffn); c.gated = d->gated;
+    uint64_t thr = 0;
+    float kp = 0;
+    rgo_keep_threshold(d->keep_prob, &thr, &kp);
+    c.keep_prob = kp; c.threshold = thr; c.rounds = static_cast<int>(d->rounds);
+    c.seed = d->seed; c.base_offset = d->base_offset;
+    c.a_qkv = d->a_qkv; c.a_proj = d->a_proj; c.a_ffn1 = d->a_ffn1; c.a_ffn2 = d->a_ffn2;
+    c.s_attn = d->s_attn; c.s_proj = d->s_proj; c.s_ffn1 = d->s_ffn1; c.s_ffn2 = d->s_ffn2;
+    c.rng_grid = d->rng_launch.grid; c.rng_block = d->rng_launch.block; c.rng_smem = d->rng_launch.dyn_smem;
+    rgo::BlockBuffers bb{b->x, b->wqkv, b->wo, b->w1, b->w2, b->qkv, b->attn_o, b->attn_o8, b->y1, b->h,
+                         b->mask, b->mask_bytes, b->counter, b->lse};
+    rgo::Block* impl = nullptr;
+    cudaError_t ce = rgo::block_create(c, bb, mode, d->use_graph != 0, &impl);
+    if (ce != cudaSuccess) return cuda_fail(ce, "rgo_block_create");
+    *out = new rgo_block{impl};
+    return RGO_OK;
+}
+
+int rgo_block_step(rgo_block* blk, rgo_stream_t stream, int32_t* launches) {
+    if (!blk) return fail(RGO_EINVAL, "rgo_block_step: null handle");
+    int n = 0;
+    cudaError_t ce = rgo::block_step(blk->impl, static_cast<cudaStream_t>(stream), &n);
+    if (launches) *launches = n;
+    return ce == cudaSuccess ? RGO_OK : cuda_fail(ce, "rgo_block_step");
+}
+
+int rgo_block_destroy(rgo_block* blk) {
+    if (!blk) return RGO_OK;
+    rgo::block_destroy(blk->impl);
+    delete blk;
+    return RGO_OK;
 }
 
 }  // extern "C"

@@ -1,0 +1,93 @@
+"""GPU: one transformer-block step (csrc/block.cu) in each overlap mode.
+All three modes must produce bitwise-identical results (the fused and
+decoupled attention agree bitwise, GEMMs are deterministic), the mask must
+equal K1's, and every stage must match a PyTorch fp32 reference computed from
+that stage's actual inputs (FP8 <= 2e-2, BF16 <= 5e-3 relative)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    a, b = a.double(), b.double()
+    return float((a - b).norm() / b.norm())
+
+
+def small_cfg(rgo):
+    return rgo.WorkloadConfig(batch=2, seq=512, heads=4, head_dim=128, ffn_dim=384, gated=True, keep_prob=0.9,
+                              philox_rounds=10)
+
+
+def snapshot(b):
+    return {k: getattr(b, k).clone() for k in ("x", "qkv", "attn_o", "attn_o8", "y1", "h")}
+
+
+def test_modes_bitwise_identical(rgo, cuda):
+    import torch
+    cfg = small_cfg(rgo)
+    outs = {}
+    for mode in ("serial_fused", "streams", "in_gemm"):
+        b = rgo.Block(cfg, mode, seed=42, use_graph=(mode != "in_gemm"))
+        b.step()
+        torch.cuda.synchronize()
+        outs[mode] = (snapshot(b), b.mask.clone())
+        b.close()
+    base = outs["serial_fused"][0]
+    for mode in ("streams", "in_gemm"):
+        for k, v in outs[mode][0].items():
+            assert torch.equal(v.view(torch.uint8), base[k].view(torch.uint8)), (mode, k)
+    lay = rgo.MaskLayout(cfg.batch, cfg.heads, cfg.seq, 42)
+    want = rgo.generate_mask_device(lay, rgo.KeepThreshold(0.9), 10)
+    for mode in ("streams", "in_gemm"):
+        assert torch.equal(outs[mode][1], want[: outs[mode][1].numel()]), mode
+
+
+def test_block_stages_vs_torch(rgo, cuda):
+    import torch
+    import torch.nn.functional as F
+    cfg = small_cfg(rgo)
+    b = rgo.Block(cfg, "streams", seed=7)
+    attn_in = b.attn_o.clone()
+    b.step()
+    torch.cuda.synchronize()
+    d, Fd = b.d, b.F
+    w = b.weights
+    dq = b.desc
+    f8 = torch.float8_e4m3fn
+    assert rel(b.attn_o8.float(), (attn_in.float() * dq.s_attn).to(f8).float()) < 2e-2
+    y1 = (b.attn_o8.float() @ w["wo"].float().T) * dq.a_proj * dq.s_proj
+    assert rel(b.y1.float(), y1.to(f8).float()) < 2e-2
+    hh = (b.y1.float() @ w["w1"].float().T) * dq.a_ffn1
+    hh = hh.view(b.M, -1, 2, 128)
+    hact = F.silu(hh[:, :, 0]) * hh[:, :, 1] * dq.s_ffn1
+    assert rel(b.h.float(), hact.reshape(b.M, Fd).to(f8).float()) < 2e-2
+    x = (b.h.float() @ w["w2"].float().T) * dq.a_ffn2 * dq.s_ffn2
+    assert rel(b.x.float(), x.to(f8).float()) < 2e-2
+    qkv = (b.x.float() @ w["wqkv"].float().T) * dq.a_qkv
+    assert rel(b.qkv.float(), qkv) < 5e-3
+    # attention from the actual QKV with the stored mask
+    B, S, H, D = cfg.batch, cfg.seq, cfg.heads, cfg.head_dim
+    q, k, v = b.qkv.float().view(B, S, 3, H, D).permute(2, 0, 3, 1, 4)
+    sc = (q @ k.transpose(-1, -2)) / np.sqrt(D)
+    pr = torch.softmax(sc, -1)
+    bits = np.unpackbits(b.mask.cpu().numpy(), bitorder="little")[: B * H * S * S]
+    keep = torch.from_numpy(bits.reshape(B, H, S, S).astype(np.float32)).cuda()
+    o = ((pr * keep / np.float32(0.9)) @ v).permute(0, 2, 1, 3).reshape(B * S, d)
+    assert rel(b.attn_o.float(), o) < 5e-3
+    b.close()
+
+
+def test_graph_replay_is_deterministic(rgo, cuda):
+    import torch
+    cfg = small_cfg(rgo)
+    b1 = rgo.Block(cfg, "streams", seed=3, use_graph=True)
+    b2 = rgo.Block(cfg, "streams", seed=3, use_graph=False)
+    for _ in range(3):
+        b1.step()
+        b2.step()
+    torch.cuda.synchronize()
+    for k in ("x", "qkv", "attn_o"):
+        assert torch.equal(getattr(b1, k).view(torch.uint8), getattr(b2, k).view(torch.uint8)), k
+    b1.close()
+    b2.close()
