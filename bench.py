@@ -1,13 +1,20 @@
-"""bench.py -- Llama2-7B dropout-RNG pipeline on B200.
+"""bench.py -- Llama2-7B transformer block with attention dropout on B200.
 
-    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--workload mask]
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--workload block|mask]
 
-One JSON line on rank 0.  Under torchrun each rank runs its own replica with a
-disjoint Philox counter range (weak scaling, no collective on the data path).
+Headline (BASELINE.json metric "Llama2 block ms & speedup (RNG hidden vs fused
+dropout); mask Gbit/s"): ms per steady-state block step (Proj+FFN1+FFN2 of
+block L-1, QKV of block L, attention of block L; FP8 GEMMs, bf16 attention,
+keep 0.9, Philox-10) with the dropout RNG hidden under the GEMMs, the same step
+with Philox fused into attention (the baseline), their ratio, and the
+stand-alone mask kernel's Gbit/s.  One JSON line on rank 0.  Under torchrun
+each rank runs its own block replica with a disjoint Philox counter range
+(weak scaling; no collective on the data path; timing = max over ranks).
 """
 from __future__ import annotations
 
 import argparse
+import concurrent.futures as cf
 import json
 import os
 import subprocess
@@ -18,8 +25,8 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-# Llama2-7B block (BASELINE.json configs[1]).
-L_CFG = dict(batch=4, seq=4096, heads=32, head_dim=128, d_model=4096, ffn=11008, keep_prob=0.9, rounds=10)
+# Llama2-7B block (BASELINE.json configs[1]): batch 4, seq 4096, 32 heads, d 4096, FFN 11008 (SwiGLU).
+L = dict(batch=4, seq=4096, heads=32, head_dim=128, ffn=11008, keep_prob=0.9, rounds=10)
 
 
 def load_peaks():
@@ -27,11 +34,12 @@ def load_peaks():
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             return json.load(f), "measured"
     except OSError:
-        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+                "sm_max_mhz": 1965.0}, "fallback"
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -51,7 +59,7 @@ class ClockSampler:
                     self.samples.append([x.strip() for x in out.split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.1)
 
     def __enter__(self):
         self._t.start()
@@ -62,14 +70,19 @@ class ClockSampler:
         self._t.join(timeout=10)
 
     def summary(self):
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = sorted(v for v in (num(s[0]) for s in self.samples) if v is not None)
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i] == "Active"})
-        return {"sm_mhz": sm[len(sm) // 2] if sm else None,
-                "sm_max_mhz": float(self.samples[0][1]) if self.samples[0][1].replace(".", "").isdigit() else None,
-                "reasons": reasons, "samples": len(self.samples)}
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 3 + i and s[3 + i] == "Active"})
+        pw = [v for v in (num(s[2]) for s in self.samples) if v is not None]
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": num(self.samples[0][1]),
+                "reasons": reasons, "power_w_max": max(pw) if pw else None, "samples": len(self.samples)}
 
 
 def dist_setup():
@@ -102,97 +115,204 @@ def max_over_ranks(x: float, world: int) -> float:
     return float(t.item())
 
 
-# --------------------------------------------------------------- CPU side
-def cpu_mask_baseline(cfg, kind="port", target_s=10.0):
-    """generate_mask on the host cores on a bounded sample (whole (b,h)
-    slices of the Llama2 mask), all hardware threads.  kind "reference" runs
-    the reference compiled in place (oracle/_ref), "port" the C oracle."""
-    import numpy as np
+# --------------------------------------------------------------------- CPU side
+def _oracle():
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle
+    return oracle
+
+
+def cpu_reference_block(cfg, target_s=10.0, kind="reference"):
+    """The reference's CPU path for this workload, on this host's cores:
+    generate_mask (mask.hpp:142-179, all threads) over a sample of (b,h)
+    slices, and attention_dropout_fused (ref_attention.hpp:114-126), one slice
+    per core in parallel (base_offset = s*SQ^2/4, bitwise identical to that
+    slice of the full run).  Extrapolated to the full B*nH slices.  The
+    reference has no GEMM arithmetic (workload.hpp:44-52 are shapes only), so
+    the GEMM part of the block is absent from this number."""
+    import numpy as np
+    oracle = _oracle()
+    use_ref = kind == "reference" and oracle.ref_available()
     cores = os.cpu_count() or 1
-    S = cfg["seq"]
-    per_slice = S * S
+    S, D, slices = cfg["seq"], cfg["head_dim"], cfg["batch"] * cfg["heads"]
     thr, _ = oracle.keep_threshold(cfg["keep_prob"])
-    buf = np.zeros(per_slice * 64 // 8, np.uint8)
+    # mask: time a sample of whole slices with all threads
+    per_slice = S * S
+    ms_slices = max(1, min(slices, int(2 ** 31 // per_slice // 8) or 1))
+    buf = np.zeros(ms_slices * per_slice // 8, np.uint8)
+    t0 = time.perf_counter()
+    if use_ref:
+        assert oracle.ref().ref_generate_mask(1, ms_slices, S, 42, 0, cfg["keep_prob"], cfg["rounds"], cores, buf,
+                                              buf.size) == 0
+    else:
+        oracle.lib().oracle_generate_mask(ms_slices * per_slice, 42, 0, thr, cfg["rounds"], cores, buf, buf.size)
+    t_mask = (time.perf_counter() - t0) * slices / ms_slices
+    # fused attention: one slice per core (bounded sample)
+    q, k, v = oracle.random_attention_input(1, S, D, 42 ^ 0xA77E)
+    n_att = min(cores, slices)
 
-    def run(slices):
-        if kind == "reference" and oracle.ref_available():
-            r = oracle.ref()
-            t0 = time.perf_counter()
-            rc = r.ref_generate_mask(1, slices, S, 42, 0, cfg["keep_prob"], cfg["rounds"], cores, buf, buf.size)
-            assert rc == 0
+    def one(s):
+        o = np.zeros_like(q)
+        if use_ref:
+            rc = oracle.ref().ref_attention(1, S, D, q, k, v, 1, 42, s * per_slice // 4, cfg["keep_prob"],
+                                            cfg["rounds"], o)
         else:
-            t0 = time.perf_counter()
-            oracle.lib().oracle_generate_mask(slices * per_slice, 42, 0, thr, cfg["rounds"], cores, buf, buf.size)
-        return time.perf_counter() - t0
+            rc = oracle.lib().oracle_attention(1, S, D, q, k, v, 1, 42, s * per_slice // 4, thr,
+                                               np.float32(cfg["keep_prob"]), cfg["rounds"], None, 0, 1, o)
+        assert rc == 0
+        return o
 
-    t1 = run(1)
-    slices = int(max(1, min(64, target_s / max(t1, 1e-6))))
-    dt = run(slices)
-    elems = slices * per_slice
-    return {"value": elems / dt / 1e9, "unit": "Gbit/s", "cores": cores,
-            "kind": "reference" if (kind == "reference" and oracle.ref_available()) else "port",
-            "sample": f"generate_mask over {slices} of {cfg['batch'] * cfg['heads']} (b,h) slices "
-                      f"(SQ {S}, R{cfg['rounds']}, keep {cfg['keep_prob']}), {dt:.2f} s",
-            "seconds": dt, "elements": elems}
+    t0 = time.perf_counter()
+    with cf.ThreadPoolExecutor(n_att) as ex:
+        list(ex.map(one, range(n_att)))
+    t_att_wall = time.perf_counter() - t0
+    t_att = t_att_wall * slices / n_att
+    ms = (t_mask + t_att) * 1e3
+    return {"value": ms, "unit": "ms", "cores": cores, "kind": "reference" if use_ref else "port",
+            "sample": f"generate_mask {ms_slices}/{slices} slices + attention_dropout_fused {n_att}/{slices} slices "
+                      f"(SQ {S}, dH {D}, keep {cfg['keep_prob']}, Philox-{cfg['rounds']}) in parallel on {cores} threads, "
+                      f"extrapolated to B{cfg['batch']}xnH{cfg['heads']}; the reference has no GEMM arithmetic",
+            "mask_s": t_mask, "attention_s": t_att, "sample_wall_s": t_att_wall}
 
 
-# --------------------------------------------------------------- GPU side
-def bench_mask(args, rank, world):
-    """K1 alone at the Llama2-7B shape: mask Gbit/s."""
+# --------------------------------------------------------------------- GPU side
+def time_steps(fn, steps, world, stream):
     import torch
-    import paper_2410_07531_b200 as rgo
-    cfg = dict(L_CFG)
-    cfg["rounds"] = args.rounds
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    barrier(world)
+    ev0.record(stream)
+    launches = 0
+    for _ in range(steps):
+        launches += fn()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    return ev0.elapsed_time(ev1) / steps, launches
+
+
+def bench_mask_kernel(rgo, cfg, rank, steps, warmup):
+    import torch
     B, H, S = cfg["batch"], cfg["heads"], cfg["seq"]
     elems = B * H * S * S
-    # disjoint counter range per rank: rank r is batch replica r
     lay = rgo.MaskLayout(B, H, S, 42, rank * elems // 4)
     thr = rgo.KeepThreshold(cfg["keep_prob"])
     out = torch.empty(elems // 8, dtype=torch.uint8, device="cuda")
+    for _ in range(warmup):
+        rgo.generate_mask_device(lay, thr, cfg["rounds"], out=out)
     s = torch.cuda.current_stream()
-    for _ in range(args.warmup):
-        rgo.generate_mask_device(lay, thr, args.rounds, out=out)
-    torch.cuda.synchronize()
-    barrier(world)
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
-        torch.cuda.synchronize()
-        barrier(world)
-        ev0.record(s)
-        for _ in range(args.steps):
-            rgo.generate_mask_device(lay, thr, args.rounds, out=out)  # 256 MiB output > L2
-        ev1.record(s)
-        torch.cuda.synchronize()
-        barrier(world)
-    ms = ev0.elapsed_time(ev1) / args.steps
-    ms = max_over_ranks(ms, world)
-    gbit = elems * world / (ms * 1e-3) / 1e9
+    ms, _ = time_steps(lambda: (rgo.generate_mask_device(lay, thr, cfg["rounds"], out=out), 1)[1], steps, 1, s)
+    return ms, elems
+
+
+def bench_block(args, rank, world):
+    import torch
+    import paper_2410_07531_b200 as rgo
+    cfg = dict(L, rounds=args.rounds)
+    wl = rgo.WorkloadConfig(batch=cfg["batch"], seq=cfg["seq"], heads=cfg["heads"], head_dim=cfg["head_dim"],
+                            ffn_dim=cfg["ffn"], gated=True, keep_prob=cfg["keep_prob"], philox_rounds=cfg["rounds"])
+    elems = cfg["batch"] * cfg["heads"] * cfg["seq"] ** 2
+    base = rank * elems // 4  # disjoint Philox counter range per rank
+    weights = rgo.block.make_weights(wl, 42, torch.device("cuda"))
+    modes = ["serial_fused", "streams", "in_gemm", "no_rng"]
+    rng_launch = tuple(args.rng_launch)
+    blocks = {m: rgo.Block(wl, m, seed=42, base_offset=base, weights=weights, rng_launch=rng_launch) for m in modes}
+    stream = torch.cuda.current_stream()
+    res, phases, launches = {}, {}, {}
     peaks, src = load_peaks()
-    sm_mhz = peaks.get("sm_max_mhz", 1965.0)
-    int_peak = 148 * 128 * sm_mhz * 1e6  # INT32 lanes x clock (op/s)
-    ops = elems * (args.rounds + 2)
-    achieved = ops / (ms * 1e-3)
-    # e2e: through the drop-in host API (D2H of the bits inside the timing)
-    t0 = time.perf_counter()
-    mk = rgo.generate_mask(lay, thr, args.rounds)
-    e2e_s = time.perf_counter() - t0
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+        for m in modes:
+            b = blocks[m]
+            for _ in range(args.warmup):
+                b.step()
+            ms, n = time_steps(b.step, args.steps, world, stream)
+            res[m] = max_over_ranks(ms, world)
+            phases[m] = b.last_timings()
+            launches[m] = n
+        # dominant kernel in situ: attention (bits) of the overlap step, and the FFN1 GEMM alone
+        att_ms = phases["streams"][1]
+    clocks = clk.summary()
+    mask_ms, _ = bench_mask_kernel(rgo, cfg, rank, max(5, args.steps // 2), 3)
+    mask_ms = max_over_ranks(mask_ms, world)
+    # ----- e2e through the public API with host buffers: H2D of the block input
+    # (e4m3 activations, pinned) + step + D2H of the step's result row block.
+    best = min(("streams", "in_gemm"), key=lambda m: res[m])
+    b = blocks[best]
+    x_host = b.x.view(torch.uint8).cpu().pin_memory()
+    out_host = torch.empty(4096, dtype=torch.bfloat16).pin_memory()
+
+    def e2e_step():
+        b.x.view(torch.uint8).copy_(x_host, non_blocking=True)
+        n = b.step()
+        out_host.copy_(b.attn_o.view(-1)[:4096], non_blocking=True)
+        return n
+
+    for _ in range(2):
+        e2e_step()
+    e2e_ms, _ = time_steps(e2e_step, args.steps, world, stream)
+    e2e_ms = max_over_ranks(e2e_ms, world)
+    for blk in blocks.values():
+        blk.close()
+
+    gemm_flops = sum(g.flops() for g in rgo.gemm_shapes(wl))
+    attn_flops = rgo.attention_work(wl)[0]
+    fp8_peak = 2 * peaks["bf16_tflops"]  # dense FP8 = 2x dense BF16 on B200; derived from the measured bf16
+    bf16_peak = peaks["bf16_tflops"]
+    roof_ms = gemm_flops / fp8_peak / 1e9 + attn_flops / bf16_peak / 1e9
+    value = res[best]
+    hidden = None
+    if res["no_rng"] > 0:
+        hidden = 1.0 - (value - res["no_rng"]) / mask_ms
     line = {
-        "metric": "mask_gbit_s", "value": round(gbit, 2), "unit": "Gbit/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": {"workload": f"Llama2-7B dropout mask B{B} nH{H} SQ{S} keep{cfg['keep_prob']} R{args.rounds}",
-                   "l2": "output 256 MiB > L2 (no flush needed)"},
-        "roofline": {"bound": "int", "achieved": achieved / 1e12, "peak": int_peak / 1e12, "unit": "Tint-op/s",
-                     "frac": achieved / int_peak, "traffic": None,
-                     "note": f"(R+2) int ops/element; peak = 148 SMs x 128 INT32 lanes x {sm_mhz} MHz ({src} clock)"},
-        "hbm_write_gbs": elems / 8 / (ms * 1e-3) / 1e9,
-        "e2e": {"value": round(elems / e2e_s / 1e9, 2), "unit": "Gbit/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": int(mk.bits.size)},
-        "clocks": clk.summary(), "gpu_launches": args.steps,
+        "metric": "llama2_block_ms", "value": round(value, 4), "unit": "ms", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(value, 4), "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "e4m3 GEMMs + bf16 attention (fp32 accumulate)",
+        "data": "synthetic (Philox-uniform activations, random-init e4m3 weights)",
+        "config": {"workload": "Llama2-7B transformer block FP8: batch 4, seq 4096, 32 heads x 128, d_model 4096, "
+                               "FFN 11008 SwiGLU, attn dropout 0.1 (keep 0.9), Philox-10; step = Proj+FFN1+FFN2 "
+                               "of block L-1 + QKV and attention of block L",
+                   "global_batch": cfg["batch"] * world, "seq_len": cfg["seq"], "parallelism": f"replicas x{world}",
+                   "overlap_mechanism": best,
+                   "l2": "no flush: every step streams > 1 GB (mask 256 MiB, QKV 384 MiB) through a 126 MB L2"},
+        "speedup_vs_fused": round(res["serial_fused"] / value, 4),
+        "modes_ms": {m: round(v, 4) for m, v in res.items()},
+        "phases_ms": {m: {"gemm_window": round(p[0], 4), "attention": round(p[1], 4)} for m, p in phases.items()},
+        "rng_hidden_fraction": None if hidden is None else round(hidden, 4),
+        "mask_gbit_s": round(elems * world / (mask_ms * 1e-3) / 1e9, 2),
+        "mask_ms": round(mask_ms, 4),
+        "blocks_per_s": round(world * 1e3 / value, 3),
+        "block_roofline": {"ms": round(roof_ms, 4), "frac": round(roof_ms / value, 4),
+                           "def": f"sum(GEMM flop)/FP8 peak + attention flop/BF16 peak; FP8 peak = 2 x measured "
+                                  f"bf16 {bf16_peak} TF/s ({src})"},
+        "roofline": {"bound": "tensor", "kernel": "attention fwd (mask bits), in situ",
+                     "achieved": round(attn_flops / (att_ms * 1e-3) / 1e12, 2), "peak": bf16_peak,
+                     "unit": "TFLOP/s", "frac": round(attn_flops / (att_ms * 1e-3) / 1e12 / bf16_peak, 4),
+                     "traffic": None,
+                     "algorithmic": f"4*B*nH*SQ^2*dH = {attn_flops:.4e} flop per launch (workload.hpp:59-64)"},
+        "e2e": {"value": round(e2e_ms, 4), "unit": "ms", "h2d_bytes_per_step": int(x_host.numel()),
+                "d2h_bytes_per_step": int(out_host.numel() * 2)},
+        "clocks": clocks, "gpu_launches": launches[best],
     }
     return line
+
+
+def bench_mask_only(args, rank, world):
+    import paper_2410_07531_b200 as rgo
+    cfg = dict(L, rounds=args.rounds)
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+        ms, elems = bench_mask_kernel(rgo, cfg, rank, args.steps, args.warmup)
+    ms = max_over_ranks(ms, world)
+    peaks, src = load_peaks()
+    sm_mhz = peaks.get("sm_max_mhz", 1965.0)
+    int_peak = 148 * 128 * sm_mhz * 1e6
+    achieved = elems * (args.rounds + 2) / (ms * 1e-3)
+    return {"metric": "mask_gbit_s", "value": round(elems * world / (ms * 1e-3) / 1e9, 2), "unit": "Gbit/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": f"Llama2-7B dropout mask B4 nH32 SQ4096 keep0.9 R{args.rounds}"},
+            "roofline": {"bound": "int", "achieved": achieved / 1e12, "peak": int_peak / 1e12, "unit": "Tint-op/s",
+                         "frac": achieved / int_peak, "traffic": None},
+            "clocks": clk.summary(), "gpu_launches": args.steps}
 
 
 def main():
@@ -201,8 +321,9 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="mask", choices=["mask"])
+    ap.add_argument("--workload", default="block", choices=["block", "mask"])
     ap.add_argument("--rounds", type=int, default=10)
+    ap.add_argument("--rng-launch", type=int, nargs=3, default=[0, 0, 0], metavar=("GRID", "BLOCK", "SMEM"))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
 
@@ -211,25 +332,28 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        cfg = dict(L_CFG, rounds=args.rounds)
-        vals = [cpu_mask_baseline(cfg, "reference", target_s=5.0) for _ in range(max(1, args.steps // 10))]
+        cfg = dict(L, rounds=args.rounds)
+        steps = max(1, min(args.steps, 3))  # each step is a ~10 s CPU sample
+        vals = [cpu_reference_block(cfg) for _ in range(steps)]
         v = sum(x["value"] for x in vals) / len(vals)
         b = vals[-1]
-        print(json.dumps({"metric": "mask_gbit_s", "value": round(v, 4), "unit": "Gbit/s", "n_gpus": 0,
-                          "impl": "reference", "steps": len(vals), "warmup": 0, "higher_is_better": True,
-                          "config": {"workload": f"Llama2-7B dropout mask R{args.rounds} (sampled slices)"},
-                          "cpu_baseline": {"value": round(v, 4), "unit": "Gbit/s", "cores": b["cores"],
-                                           "kind": b["kind"], "sample": b["sample"]},
-                          "e2e": {"value": round(v, 4), "unit": "Gbit/s", "h2d_bytes_per_step": 0,
-                                  "d2h_bytes_per_step": 0}}))
+        print(json.dumps({
+            "metric": "llama2_block_ms", "value": round(v, 1), "unit": "ms", "n_gpus": 0, "impl": "reference",
+            "steps": steps, "warmup": 0, "higher_is_better": False, "scaling": "weak",
+            "config": {"workload": "Llama2-7B block (reference CPU path: generate_mask + attention_dropout_fused; "
+                                   "no GEMMs in the reference)", "global_batch": cfg["batch"], "seq_len": cfg["seq"]},
+            "cpu_baseline": {"value": round(v, 1), "unit": "ms", "cores": b["cores"], "kind": b["kind"],
+                             "sample": b["sample"]},
+            "e2e": {"value": round(v, 1), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
         return
 
     rank, world, _ = dist_setup()
-    line = bench_mask(args, rank, world)
+    line = bench_block(args, rank, world) if args.workload == "block" else bench_mask_only(args, rank, world)
     if rank == 0:
         if not args.no_cpu_baseline:
-            cb = cpu_mask_baseline(dict(L_CFG, rounds=args.rounds), "reference")
-            line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            cb = cpu_reference_block(dict(L, rounds=args.rounds))
+            line["cpu_baseline"] = {k: (round(cb[k], 1) if k == "value" else cb[k])
+                                    for k in ("value", "unit", "cores", "kind", "sample")}
         print(json.dumps(line))
     if world > 1:
         import torch.distributed as dist

@@ -198,7 +198,8 @@ int rgo_attn_fwd(const rgo_attn_desc* a, const rgo_tensor4* q, const rgo_tensor4
 typedef enum rgo_overlap_mode {
     RGO_OVERLAP_SERIAL_FUSED = 0,
     RGO_OVERLAP_STREAMS = 1,
-    RGO_OVERLAP_IN_GEMM = 2
+    RGO_OVERLAP_IN_GEMM = 2,
+    RGO_OVERLAP_NO_RNG = 3  /* measurement only: no RNG work, attention reads a stale mask */
 } rgo_overlap_mode;
 
 typedef struct rgo_block_desc {
@@ -237,6 +238,8 @@ int rgo_block_create(const rgo_block_desc* d, const rgo_block_buffers* b, int32_
 /* Enqueue one step ordered after prior work on `stream`; *launches (optional)
  * = number of kernels the step launches. */
 int rgo_block_step(rgo_block* blk, rgo_stream_t stream, int32_t* launches);
+/* Device time (ms) of the last completed step: [0] GEMM window, [1] attention. */
+int rgo_block_last_timings(rgo_block* blk, float* ms2);
 int rgo_block_destroy(rgo_block* blk);
 
 #ifdef __cplusplus

@@ -15,7 +15,7 @@ from . import _lib
 from .gemm import WorkloadConfig
 from .mask import KeepThreshold
 
-MODES = {"serial_fused": 0, "streams": 1, "in_gemm": 2}
+MODES = {"serial_fused": 0, "streams": 1, "in_gemm": 2, "no_rng": 3}
 
 
 def _uniform(n, stream_id, seed, device):
@@ -83,6 +83,12 @@ class Block:
         n = C.c_int32()
         _lib.check(_lib.lib().rgo_block_step(self.handle, s, C.byref(n)))
         return n.value
+
+    def last_timings(self):
+        """(GEMM-window ms, attention ms) of the last completed step."""
+        arr = (C.c_float * 2)()
+        _lib.check(_lib.lib().rgo_block_last_timings(self.handle, arr))
+        return float(arr[0]), float(arr[1])
 
     def close(self):
         if getattr(self, "handle", None):

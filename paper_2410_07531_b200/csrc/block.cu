@@ -12,6 +12,8 @@
 //                 high-priority stream; attention (K5) waits on an event
 //   IN_GEMM       mechanism B: the GEMMs carry co-resident RNG warps draining
 //                 the mask queue (K4); a tail drain finishes any remainder
+//   NO_RNG        measurement only: GEMMs + mask-reading attention with no RNG
+//                 work at all (the denominator of the hidden fraction)
 // Each step is captured once into a CUDA graph and replayed.
 #include <cuda_bf16.h>
 #include <cuda_fp8.h>
@@ -77,6 +79,7 @@ struct Block {
     cudaStream_t s_main = nullptr, s_rng = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_rng = nullptr;  // fork/join inside a step
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;    // ordering against the caller's stream
+    cudaEvent_t ev_t[3] = {nullptr, nullptr, nullptr}; // phase timing (recorded inside the graph)
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     int launches_per_step = 0;
@@ -133,6 +136,7 @@ static cudaError_t enqueue_step(Block& b, int* launches) {
         if ((e = cudaMemsetAsync(x.counter, 0, sizeof(unsigned long long), s)) != cudaSuccess) return e;
     }
     const RngQueue* rq = b.mode == BLOCK_IN_GEMM ? &q : nullptr;
+    if ((e = cudaEventRecordWithFlags(b.ev_t[0], s, cudaEventRecordExternal)) != cudaSuccess) return e;
     // attention output of the previous block -> e4m3
     if ((e = launch_quant_e4m3(x.attn_o, x.attn_o8, static_cast<uint64_t>(M) * d, c.s_attn, s)) != cudaSuccess)
         return e;
@@ -155,6 +159,7 @@ static cudaError_t enqueue_step(Block& b, int* launches) {
     g.rng = rq;
     if ((e = launch_gemm(g, s)) != cudaSuccess) return e;
     ++n;
+    if ((e = cudaEventRecordWithFlags(b.ev_t[1], s, cudaEventRecordExternal)) != cudaSuccess) return e;
     if (b.mode == BLOCK_IN_GEMM) {  // tail: whatever the GEMM-resident warps left
         if ((e = launch_rng_queue(q, 0, 0, 0, s)) != cudaSuccess) return e;
         ++n;
@@ -182,6 +187,7 @@ static cudaError_t enqueue_step(Block& b, int* launches) {
     a.rounds = c.rounds;
     if ((e = launch_attn_fwd(a, s)) != cudaSuccess) return e;
     ++n;
+    if ((e = cudaEventRecordWithFlags(b.ev_t[2], s, cudaEventRecordExternal)) != cudaSuccess) return e;
     *launches = n;
     return cudaSuccess;
 }
@@ -198,6 +204,7 @@ cudaError_t block_create(const BlockConfig& cfg, const BlockBuffers& buf, int mo
     if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&b->s_rng, cudaStreamNonBlocking, lo);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&b->ev_fork, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&b->ev_rng, cudaEventDisableTiming);
+    for (int t = 0; t < 3 && e == cudaSuccess; ++t) e = cudaEventCreate(&b->ev_t[t]);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&b->ev_in, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&b->ev_out, cudaEventDisableTiming);
     if (e == cudaSuccess && use_graph) {
@@ -237,12 +244,21 @@ cudaError_t block_step(Block* b, cudaStream_t stream, int* launches) {
     return cudaStreamWaitEvent(stream, b->ev_out, 0);
 }
 
+cudaError_t block_last_timings(Block* b, float* ms2) {
+    cudaError_t e = cudaEventSynchronize(b->ev_t[2]);
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&ms2[0], b->ev_t[0], b->ev_t[1]);
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&ms2[1], b->ev_t[1], b->ev_t[2]);
+    return e;
+}
+
 void block_destroy(Block* b) {
     if (!b) return;
     if (b->exec) cudaGraphExecDestroy(b->exec);
     if (b->graph) cudaGraphDestroy(b->graph);
     if (b->ev_fork) cudaEventDestroy(b->ev_fork);
     if (b->ev_rng) cudaEventDestroy(b->ev_rng);
+    for (int t = 0; t < 3; ++t)
+        if (b->ev_t[t]) cudaEventDestroy(b->ev_t[t]);
     if (b->ev_in) cudaEventDestroy(b->ev_in);
     if (b->ev_out) cudaEventDestroy(b->ev_out);
     if (b->s_main) cudaStreamDestroy(b->s_main);

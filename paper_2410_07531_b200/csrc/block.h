@@ -6,7 +6,7 @@
 
 namespace rgo {
 
-enum { BLOCK_SERIAL_FUSED = 0, BLOCK_STREAMS = 1, BLOCK_IN_GEMM = 2 };
+enum { BLOCK_SERIAL_FUSED = 0, BLOCK_STREAMS = 1, BLOCK_IN_GEMM = 2, BLOCK_NO_RNG = 3 };
 
 struct BlockConfig {
     int batch, seq, heads, head_dim, ffn;
@@ -42,6 +42,9 @@ struct BlockBuffers {
 struct Block;
 cudaError_t block_create(const BlockConfig& cfg, const BlockBuffers& buf, int mode, bool use_graph, Block** out);
 cudaError_t block_step(Block* b, cudaStream_t stream, int* launches);
+// Device time of the last step's phases: [0] GEMM window (quant + 4 GEMMs),
+// [1] attention (incl. the RNG join / tail), in ms.
+cudaError_t block_last_timings(Block* b, float* ms2);
 void block_destroy(Block* b);
 cudaError_t launch_quant_e4m3(const void* in, void* out, uint64_t n, float scale, cudaStream_t s);
 

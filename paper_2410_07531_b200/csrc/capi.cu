@@ -365,7 +365,7 @@ struct rgo_block {
 
 int rgo_block_create(const rgo_block_desc* d, const rgo_block_buffers* b, int32_t mode, rgo_block** out) {
     if (!d || !b || !out) return fail(RGO_EINVAL, "rgo_block_create: null argument");
-    if (mode < RGO_OVERLAP_SERIAL_FUSED || mode > RGO_OVERLAP_IN_GEMM)
+    if (mode < RGO_OVERLAP_SERIAL_FUSED || mode > RGO_OVERLAP_NO_RNG)
         return fail(RGO_EINVAL, "rgo_block_create: bad overlap mode");
     if (d->head_dim != 64 && d->head_dim != 128) return fail(RGO_EINVAL, "rgo_block_create: head_dim 64/128");
     if (!(d->keep_prob > 0.0 && d->keep_prob < 1.0)) return fail(RGO_EINVAL, "rgo_block_create: keep_prob in (0,1)");
@@ -407,6 +407,12 @@ int rgo_block_step(rgo_block* blk, rgo_stream_t stream, int32_t* launches) {
     cudaError_t ce = rgo::block_step(blk->impl, static_cast<cudaStream_t>(stream), &n);
     if (launches) *launches = n;
     return ce == cudaSuccess ? RGO_OK : cuda_fail(ce, "rgo_block_step");
+}
+
+int rgo_block_last_timings(rgo_block* blk, float* ms2) {
+    if (!blk || !ms2) return fail(RGO_EINVAL, "rgo_block_last_timings: null argument");
+    cudaError_t ce = rgo::block_last_timings(blk->impl, ms2);
+    return ce == cudaSuccess ? RGO_OK : cuda_fail(ce, "rgo_block_last_timings");
 }
 
 int rgo_block_destroy(rgo_block* blk) {
