@@ -101,6 +101,16 @@ static GemmJob gemm(const BlockConfig& c, int M, int N, int K, const void* A, co
     return j;
 }
 
+// Phase-timing events: inside a graph capture they must be external event
+// record nodes; in eager mode a plain record.
+static cudaError_t record_timing(Block& b, int i, cudaStream_t s) {
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    cudaError_t e = cudaStreamIsCapturing(s, &st);
+    if (e != cudaSuccess) return e;
+    return st == cudaStreamCaptureStatusActive ? cudaEventRecordWithFlags(b.ev_t[i], s, cudaEventRecordExternal)
+                                               : cudaEventRecord(b.ev_t[i], s);
+}
+
 // Enqueue one step on b.s_main (+ b.s_rng); returns #kernels launched.
 static cudaError_t enqueue_step(Block& b, int* launches) {
     const BlockConfig& c = b.cfg;
@@ -125,9 +135,12 @@ static cudaError_t enqueue_step(Block& b, int* launches) {
         if ((e = cudaEventRecord(b.ev_fork, s)) != cudaSuccess) return e;
         if ((e = cudaStreamWaitEvent(b.s_rng, b.ev_fork, 0)) != cudaSuccess) return e;
         MaskJob mj{x.mask, elems, c.seed, c.base_offset, c.threshold, c.rounds};
+        // Default shape: one 256-thread CTA per SM.  With a GEMM CTA resident
+        // (192 threads, ~31K registers, 198 KB smem) exactly one such CTA fits
+        // beside it, and spread one per SM it can never crowd a GEMM CTA out.
         LaunchShape ls;
-        ls.grid = c.rng_grid;
-        ls.block = c.rng_block;
+        ls.grid = c.rng_grid ? c.rng_grid : static_cast<unsigned>(num_sms());
+        ls.block = c.rng_block ? c.rng_block : 256;
         ls.dyn_smem = c.rng_smem;
         if ((e = launch_mask(mj, ls, b.s_rng)) != cudaSuccess) return e;
         ++n;
@@ -136,7 +149,7 @@ static cudaError_t enqueue_step(Block& b, int* launches) {
         if ((e = cudaMemsetAsync(x.counter, 0, sizeof(unsigned long long), s)) != cudaSuccess) return e;
     }
     const RngQueue* rq = b.mode == BLOCK_IN_GEMM ? &q : nullptr;
-    if ((e = cudaEventRecordWithFlags(b.ev_t[0], s, cudaEventRecordExternal)) != cudaSuccess) return e;
+    if ((e = record_timing(b, 0, s)) != cudaSuccess) return e;
     // attention output of the previous block -> e4m3
     if ((e = launch_quant_e4m3(x.attn_o, x.attn_o8, static_cast<uint64_t>(M) * d, c.s_attn, s)) != cudaSuccess)
         return e;
@@ -159,7 +172,7 @@ static cudaError_t enqueue_step(Block& b, int* launches) {
     g.rng = rq;
     if ((e = launch_gemm(g, s)) != cudaSuccess) return e;
     ++n;
-    if ((e = cudaEventRecordWithFlags(b.ev_t[1], s, cudaEventRecordExternal)) != cudaSuccess) return e;
+    if ((e = record_timing(b, 1, s)) != cudaSuccess) return e;
     if (b.mode == BLOCK_IN_GEMM) {  // tail: whatever the GEMM-resident warps left
         if ((e = launch_rng_queue(q, 0, 0, 0, s)) != cudaSuccess) return e;
         ++n;
@@ -187,7 +200,7 @@ static cudaError_t enqueue_step(Block& b, int* launches) {
     a.rounds = c.rounds;
     if ((e = launch_attn_fwd(a, s)) != cudaSuccess) return e;
     ++n;
-    if ((e = cudaEventRecordWithFlags(b.ev_t[2], s, cudaEventRecordExternal)) != cudaSuccess) return e;
+    if ((e = record_timing(b, 2, s)) != cudaSuccess) return e;
     *launches = n;
     return cudaSuccess;
 }

@@ -1,0 +1,35 @@
+"""Sweep the mechanism-A mask-kernel launch shape and compare with mechanism B."""
+import json, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2410_07531_b200 as rgo
+
+wl = rgo.WorkloadConfig(batch=4, seq=4096, heads=32, head_dim=128, ffn_dim=11008, gated=True, keep_prob=0.9,
+                        philox_rounds=int(os.environ.get("ROUNDS", "10")))
+weights = rgo.block.make_weights(wl, 42, torch.device("cuda"))
+
+
+def run(mode, launch=(0, 0, 0), steps=10):
+    b = rgo.Block(wl, mode, seed=42, weights=weights, rng_launch=launch)
+    for _ in range(3):
+        b.step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        b.step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    ph = b.last_timings()
+    b.close()
+    print(json.dumps({"mode": mode, "launch": launch, "ms": round(ms, 4), "gemm_window": round(ph[0], 4),
+                      "attention": round(ph[1], 4)}), flush=True)
+
+
+run("no_rng")
+run("serial_fused")
+run("in_gemm")
+for launch in [(0, 0, 0), (148, 128, 0), (148, 256, 0), (148, 384, 0), (296, 128, 0), (296, 256, 0), (444, 128, 0),
+               (74, 256, 0)]:
+    run("streams", launch)
