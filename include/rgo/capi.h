@@ -186,6 +186,46 @@ int rgo_attn_fwd(const rgo_attn_desc* a, const rgo_tensor4* q, const rgo_tensor4
                  const rgo_tensor4* v, const uint8_t* d_bits, uint64_t bits_bytes,
                  const rgo_tensor4* o, float* d_lse, rgo_stream_t stream);
 
+/* ------------------------------------------------------ host-buffer entry --
+ * Drop-in forms of the reference's value-semantics API: host arrays in and
+ * out, the library stages them through device memory it allocates and frees
+ * inside the call (computation is on the GPU; there is no CPU path). */
+
+/* n x philox_block on host arrays (keys n x 2, ctrs n x 4, rounds n, out n x 4). */
+int rgo_philox_blocks_host(const uint32_t* h_keys, const uint32_t* h_ctrs, const int32_t* h_rounds,
+                           uint32_t* h_out, uint64_t n);
+
+/* random_attention_input (ref_attention.hpp:176-207): three float arrays of
+ * slices*seq*head_dim values (q: stream 1, k: 2, v: 3). */
+int rgo_random_attention_input_host(uint32_t slices, uint32_t seq, uint32_t head_dim, uint64_t seed,
+                                    float* h_q, float* h_k, float* h_v);
+
+/* attention_forward / _fused / _decoupled on reference-layout float arrays
+ * (slice, pos, dim), any head_dim <= 128 (zero-padded to 64/128 on device;
+ * the softmax scale stays 1/sqrt(head_dim)).  Inputs are rounded to bf16 for
+ * the tensor cores; h_bits is the packed mask for RGO_MASK_BITS. */
+typedef struct rgo_attn_host_desc {
+    uint32_t slices, seq, head_dim;
+    int32_t mask_source;  /* rgo_mask_source */
+    double keep_prob;
+    uint64_t seed, base_offset;
+    uint32_t rounds;
+    uint32_t reserved;
+} rgo_attn_host_desc;
+
+int rgo_attention_host(const rgo_attn_host_desc* a, const float* h_q, const float* h_k,
+                       const float* h_v, const uint8_t* h_bits, uint64_t bits_bytes, float* h_o);
+
+/* RNGM mask file (mask.hpp:188-297): 40-byte little-endian header
+ * (magic "RNGM", u16 version 1, u16 rounds, u32 B, nH, SQ, u64 seed,
+ * base_offset, f32 keep_prob) + packed payload.  Load validates magic,
+ * version, rounds, truncation and padding bits (RGO_EIO on failure);
+ * call with h_bits = NULL to read the header and required payload size. */
+int rgo_mask_save(const char* path, const rgo_mask_desc* d, float keep_prob, const uint8_t* h_bits,
+                  uint64_t bytes);
+int rgo_mask_load(const char* path, rgo_mask_desc* d, float* keep_prob, uint8_t* h_bits,
+                  uint64_t capacity, uint64_t* bytes);
+
 /* ----------------------------------------------------------------- block --
  * Transformer-block step (the paper's timeline, schedule.hpp:111-136): the
  * four GEMMs between consecutive attention layers (Proj, FFN1, FFN2 of block

@@ -126,6 +126,15 @@ SIGNATURES = {
     "rgo_block_step": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "rgo_block_last_timings": (C.c_int, [C.c_void_p, C.c_void_p]),
     "rgo_block_destroy": (C.c_int, [C.c_void_p]),
+    "rgo_philox_blocks_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64]),
+    "rgo_random_attention_input_host": (
+        C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "rgo_attention_host": (
+        C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
+    "rgo_mask_save": (C.c_int, [C.c_char_p, C.POINTER(mask_desc), C.c_float, C.c_void_p, C.c_uint64]),
+    "rgo_mask_load": (
+        C.c_int, [C.c_char_p, C.POINTER(mask_desc), C.POINTER(C.c_float), C.c_void_p, C.c_uint64,
+                  C.POINTER(C.c_uint64)]),
     "rgo_uniform_fill": (
         C.c_int,
         [C.c_uint64, C.c_uint32, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p],

@@ -67,6 +67,10 @@ namespace rgo {
 cudaError_t launch_quant_e4m3(const void* in, void* out, uint64_t n, float scale, cudaStream_t s) {
     const uint64_t threads = (n + 15) / 16;
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((threads + 255) / 256, 148 * 16));
+    static bool once = (cudaFuncSetAttribute(rgo_dev::quant_e4m3_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                             cudaSharedmemCarveoutMaxShared),
+                        true);
+    (void)once;
     rgo_dev::quant_e4m3_kernel<<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(in),
                                                     static_cast<uint8_t*>(out), n, scale);
     return cudaGetLastError();

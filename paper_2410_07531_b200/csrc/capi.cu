@@ -81,6 +81,12 @@ int num_sms() {
 
 extern "C" {
 
+// internal: lets the other translation units report through rgo_last_error()
+int rgo_internal_set_error(int code, const char* msg) {
+    std::snprintf(g_err, sizeof g_err, "%s", msg);
+    return code;
+}
+
 const char* rgo_last_error(void) { return g_err; }
 
 int rgo_version(void) { return 1; }

@@ -96,9 +96,23 @@ __global__ void mask_fill_kernel(uint8_t* __restrict__ out, uint64_t n, uint8_t 
 }
 
 // Generic R in [1,16] via a switch over template instances.
+// The mask kernels use no shared memory, but an SM's L1/shared split is chosen
+// when CTAs are placed and cannot change while any CTA is resident: a kernel
+// that lets the driver pick a small carveout would lock a concurrently
+// launched GEMM / attention CTA (~200 KB smem) out of every SM it occupies,
+// serialising the "overlap".  Preferring the maximum carveout keeps the SMs
+// configured for the tensor-core kernels, so the two really co-reside.
+template <typename K>
+static void prefer_max_smem(K kernel) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+}
+
 template <int R>
 static cudaError_t launch_r(uint8_t* out, uint64_t n_vec, uint64_t base, uint32_t k0, uint32_t k1,
                             uint32_t thr, const rgo::LaunchShape& ls, cudaStream_t s) {
+    static bool once = (prefer_max_smem(rng_mask_kernel<R>), true);
+    (void)once;
     rng_mask_kernel<R><<<ls.grid, ls.block, ls.dyn_smem, s>>>(out, n_vec, base, k0, k1, thr, 0u);
     return cudaGetLastError();
 }
@@ -142,6 +156,8 @@ cudaError_t launch_mask(const MaskJob& j, const LaunchShape& shape_in, cudaStrea
         const uint64_t nbytes = (n + 7) / 8;
         const uint64_t blocks = (nbytes + 255) / 256;
         const unsigned grid = static_cast<unsigned>(blocks < 148 * 8 ? blocks : 148 * 8);
+        static bool once = (prefer_max_smem(mask_fill_kernel), true);
+        (void)once;
         mask_fill_kernel<<<grid, 256, 0, s>>>(j.out, n, j.threshold ? 0xFF : 0x00);
         return cudaGetLastError();
     }
@@ -210,6 +226,9 @@ cudaError_t launch_rng_queue(const RngQueue& q, unsigned grid, unsigned block, s
             cudaFuncSetAttribute(rgo_dev::rng_queue_kernel<R>,                       \
                                  cudaFuncAttributeMaxDynamicSharedMemorySize,        \
                                  static_cast<int>(dyn_smem));                        \
+        cudaFuncSetAttribute(rgo_dev::rng_queue_kernel<R>,                           \
+                             cudaFuncAttributePreferredSharedMemoryCarveout,         \
+                             cudaSharedmemCarveoutMaxShared);                        \
         rgo_dev::rng_queue_kernel<R><<<grid, block, dyn_smem, s>>>(q);               \
         break;
         RGO_CASE(1) RGO_CASE(2) RGO_CASE(3) RGO_CASE(4) RGO_CASE(5) RGO_CASE(6) RGO_CASE(7)
