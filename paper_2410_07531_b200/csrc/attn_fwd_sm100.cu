@@ -124,6 +124,14 @@ __device__ __forceinline__ void keep_bits(const AttnParams& p, uint64_t idx0, ui
     }
 }
 
+// 2^x on the SFU (MUFU.EX2, flush-to-zero): exp2f() adds range fix-ups that
+// cost several ALU instructions per element.
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 template <int HD, int MODE, int R>
 __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ,
                                                               const __grid_constant__ CUtensorMap tmK,
@@ -287,21 +295,27 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(const __grid_const
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
             for (int c = 0; c < 4; ++c) reg_fence(s[c]);
-            const int valid = p.S - j0;  // columns >= valid are padding
-            float tmax = -INFINITY;
+            const int valid = p.S - j0;  // columns >= valid are padding (last tile only)
+            if (valid < BKV) {               // warp-uniform: the slow path runs once per row
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+#pragma unroll
+                    for (int e = 0; e < 32; ++e)
+                        if (c * 32 + e >= valid) s[c][e] = __float_as_uint(-INFINITY);
+            }
+            // raw row max (scale > 0 commutes with max): 3-input FMNMX
+            float mx0 = -INFINITY, mx1 = -INFINITY;
 #pragma unroll
             for (int c = 0; c < 4; ++c)
 #pragma unroll
-                for (int e = 0; e < 32; ++e) {
-                    float t = __uint_as_float(s[c][e]) * p.scale_log2;
-                    if (c * 32 + e >= valid) t = -INFINITY;
-                    s[c][e] = __float_as_uint(t);
-                    tmax = fmaxf(tmax, t);
+                for (int e = 0; e < 32; e += 4) {
+                    mx0 = fmaxf(mx0, fmaxf(__uint_as_float(s[c][e]), __uint_as_float(s[c][e + 1])));
+                    mx1 = fmaxf(mx1, fmaxf(__uint_as_float(s[c][e + 2]), __uint_as_float(s[c][e + 3])));
                 }
-            const float m_new = fmaxf(m, tmax);
+            const float m_new = fmaxf(m, fmaxf(mx0, mx1) * p.scale_log2);
             const bool need = m_new > m + RESCALE_THRESHOLD;
             if (__any_sync(0xffffffffu, need)) {
-                const float alpha = exp2f(m - m_new);  // 0 on the first tile
+                const float alpha = ex2_approx(m - m_new);  // 0 on the first tile
                 if (j > 0) {
 #pragma unroll 1
                     for (int c = 0; c < HD / 32; ++c) {
@@ -316,7 +330,11 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(const __grid_const
                 l *= alpha;
                 m = m_new;
             }
-            float rs = 0.0f;
+            // p = 2^(s*scale - m): one packed FFMA2 + two MUFU.EX2 per pair; the
+            // row sum (over ALL keys, before dropout) with packed FADD2.
+            const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
+            const float2 nm2 = make_float2(-m, -m);
+            float2 rs2 = make_float2(0.0f, 0.0f);
 #pragma unroll
             for (int h = 0; h < 2; ++h) {  // P columns [64h, 64h+64) -> TMEM cols [32h, 32h+32)
                 uint32_t pk[32];
@@ -325,17 +343,21 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(const __grid_const
                     const int c = 2 * h + cc;
 #pragma unroll
                     for (int e = 0; e < 32; e += 2) {
-                        float p0 = exp2f(__uint_as_float(s[c][e]) - m);
-                        float p1 = exp2f(__uint_as_float(s[c][e + 1]) - m);
-                        rs += p0 + p1;
-                        if (!((kw[c] >> e) & 1u)) p0 = 0.0f;
-                        if (!((kw[c] >> (e + 1)) & 1u)) p1 = 0.0f;
+                        const float2 t2 = __ffma2_rn(make_float2(__uint_as_float(s[c][e]), __uint_as_float(s[c][e + 1])),
+                                                     sc2, nm2);
+                        float p0 = ex2_approx(t2.x), p1 = ex2_approx(t2.y);
+                        rs2 = __fadd2_rn(rs2, make_float2(p0, p1));
+                        if (MODE != MASK_NONE) {
+                            p0 = ((kw[c] >> e) & 1u) ? p0 : 0.0f;
+                            p1 = ((kw[c] >> (e + 1)) & 1u) ? p1 : 0.0f;
+                        }
                         __nv_bfloat162 hv = __floats2bfloat162_rn(p0, p1);
                         pk[cc * 16 + (e >> 1)] = *reinterpret_cast<uint32_t*>(&hv);
                     }
                 }
                 tmem_st32(tS + 32 * h, pk);
             }
+            const float rs = rs2.x + rs2.y;
             l += rs;
             tmem_st_wait();
             tc_fence_before();
