@@ -36,6 +36,9 @@ __global__ void __launch_bounds__(256) rng_mask_kernel(uint8_t* __restrict__ out
                                                        uint64_t base_offset, uint32_t k0,
                                                        uint32_t k1, uint32_t thr, uint32_t zero) {
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    // key / threshold in vector registers rather than uniform registers, so a
+    // co-resident GEMM keeps the uniform datapath it issues MMAs/TMA through
+    asm volatile("" : "+r"(k0), "+r"(k1), "+r"(thr) : "r"(threadIdx.x));
     for (uint64_t v = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < n_vec;
          v += stride) {
         const uint64_t ctr = base_offset + v * 32;  // 64-bit wrap like element_source

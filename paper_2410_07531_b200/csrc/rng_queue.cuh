@@ -12,16 +12,17 @@
 
 namespace rgo {
 
+// k0/k1/thr arrive as per-thread (vector-register) copies: see rng_drain_r.
 template <int R>
-__device__ __forceinline__ void rng_vector(const RngQueue& q, uint64_t v) {
+__device__ __forceinline__ void rng_vector(const RngQueue& q, uint64_t v, uint32_t k0, uint32_t k1, uint32_t thr) {
     const uint64_t ctr = q.base_offset + v * 32;
     const uint32_t lo = static_cast<uint32_t>(ctr), hi = static_cast<uint32_t>(ctr >> 32);
     uint32_t w0, w1, w2, w3;
     if (lo <= 0xFFFFFFFFu - 31u) {
-        w0 = rgo_dev::keep32_nowrap<R>(lo + 0, hi, q.k0, q.k1, q.thr, 0u);
-        w1 = rgo_dev::keep32_nowrap<R>(lo + 8, hi, q.k0, q.k1, q.thr, 0u);
-        w2 = rgo_dev::keep32_nowrap<R>(lo + 16, hi, q.k0, q.k1, q.thr, 0u);
-        w3 = rgo_dev::keep32_nowrap<R>(lo + 24, hi, q.k0, q.k1, q.thr, 0u);
+        w0 = rgo_dev::keep32_nowrap<R>(lo + 0, hi, k0, k1, thr, 0u);
+        w1 = rgo_dev::keep32_nowrap<R>(lo + 8, hi, k0, k1, thr, 0u);
+        w2 = rgo_dev::keep32_nowrap<R>(lo + 16, hi, k0, k1, thr, 0u);
+        w3 = rgo_dev::keep32_nowrap<R>(lo + 24, hi, k0, k1, thr, 0u);
     } else {
         w0 = rgo_dev::keep32<R>(ctr + 0, q.k0, q.k1, q.thr);
         w1 = rgo_dev::keep32<R>(ctr + 8, q.k0, q.k1, q.thr);
@@ -37,6 +38,12 @@ __device__ __forceinline__ void rng_vector(const RngQueue& q, uint64_t v) {
 template <int R>
 __device__ __forceinline__ void rng_drain_r(const RngQueue& q, const volatile int* stop, int stop_at) {
     const uint32_t lane = threadIdx.x & 31;
+    // Keep the key and threshold in vector registers: left to itself the
+    // compiler holds them (and the R round keys) in uniform registers, and the
+    // RNG's LOP3/compare stream then competes for the uniform datapath that
+    // the co-resident GEMM's MMA/TMA warps issue through.
+    uint32_t k0 = q.k0, k1 = q.k1, thr = q.thr;
+    asm volatile("" : "+r"(k0), "+r"(k1), "+r"(thr) : "r"(lane));
     while (true) {
         if (stop && *stop >= stop_at) break;
         unsigned long long start = 0;
@@ -44,7 +51,7 @@ __device__ __forceinline__ void rng_drain_r(const RngQueue& q, const volatile in
         start = __shfl_sync(0xffffffffu, start, 0);
         if (start >= q.n_vec) break;
         const uint64_t v = start + lane;
-        if (v < q.n_vec) rng_vector<R>(q, v);
+        if (v < q.n_vec) rng_vector<R>(q, v, k0, k1, thr);
     }
 }
 

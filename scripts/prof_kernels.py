@@ -24,9 +24,24 @@ elif which.startswith("attn"):
         dict(mask_source=2, keep_prob=0.9, seed=42, rounds=10)
     for _ in range(3):
         rgo.attn_fwd(q, k, v, o, **kw)
-else:
+elif which == "mask":
     lay = rgo.MaskLayout(4, 32, 4096, 42)
     out = torch.empty(lay.elem_count() // 8, dtype=torch.uint8, device="cuda")
     for _ in range(3):
         rgo.generate_mask_device(lay, rgo.KeepThreshold(0.9), 10, out=out)
 torch.cuda.synchronize()
+
+if which == "gemm_rng":
+    M, N, K = 16384, 22016, 4096
+    a = (torch.rand(M, K, device="cuda") - 0.5).to(torch.float8_e4m3fn)
+    b = (torch.rand(N, K, device="cuda") - 0.5).to(torch.float8_e4m3fn)
+    c = torch.empty(M, N // 2, dtype=torch.float8_e4m3fn, device="cuda")
+    lay = rgo.MaskLayout(4, 32, 4096, 42)
+    d = rgo.mask.desc(lay, rgo.KeepThreshold(0.9), 10)
+    bits = torch.empty(lay.elem_count() // 8, dtype=torch.uint8, device="cuda")
+    counter = torch.zeros(1, dtype=torch.int64, device="cuda")
+    for _ in range(3):
+        counter.zero_()
+        rgo.gemm_with_rng(a, b, c, d, bits, counter, epilogue="swiglu", alpha=0.05)
+    torch.cuda.synchronize()
+    print("rng vectors done during one GEMM:", int(counter.item()), "of", lay.elem_count() // 128)
