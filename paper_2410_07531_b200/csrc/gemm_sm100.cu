@@ -67,10 +67,17 @@ __device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, 
     nb = local / gsize;
 }
 
-__device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
+// Epilogue activations on the SFU: x * rcp(1 + 2^(-x*log2e)) and tanh.approx
+// (IEEE division / tanhf cost ~25 instructions per element).
+__device__ __forceinline__ float silu(float x) { return __fdividef(x, 1.0f + __expf(-x)); }
+__device__ __forceinline__ float tanh_approx(float x) {
+    float y;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 __device__ __forceinline__ float gelu_tanh(float x) {
     const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-    return 0.5f * x * (1.0f + tanhf(k0 * (x + k1 * x * x * x)));
+    return 0.5f * x * (1.0f + tanh_approx(k0 * (x + k1 * x * x * x)));
 }
 
 template <int OUT>
@@ -150,40 +157,45 @@ __global__ void __launch_bounds__(CORE_THREADS + 32 * RNG_WARPS, 1)
     const int bk_elems = FP8 ? BKB : BKB / 2;
     constexpr uint32_t IDESC = FP8 ? idesc_make(0, 0, BM, BN, 0, 0) : idesc_make(1, 1, BM, BN, 0, 0);
 
-    if (warp == 0) {
-        if (lane == 0) {  // ---------------- TMA producer
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-                int mb, nb;
-                tile_coords(tile, p.tiles_m, p.tiles_n, mb, nb);
-                for (int kb = 0; kb < kblocks; ++kb) {
-                    mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
-                    const uint32_t fb = smem_u32(&full[stage]);
+    if (warp == 0) {  // ---------------- TMA producer (whole warp loops, one lane issues)
+        int stage = 0;
+        uint32_t phase = 0;
+        const uint32_t sa = smem_u32(smA), sb = smem_u32(smB), fb0 = smem_u32(&full[0]), eb0 = smem_u32(&empty[0]);
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            int mb, nb;
+            tile_coords(tile, p.tiles_m, p.tiles_n, mb, nb);
+            const int row_a = mb * BM, row_b = nb * BN;
+            for (int kb = 0; kb < kblocks; ++kb) {
+                mbar_wait(eb0 + 8 * stage, phase ^ 1);
+                if (elect_one()) {
+                    const uint32_t fb = fb0 + 8 * stage;
                     mbar_arrive_expect_tx(fb, STAGE_BYTES);
-                    tma_load_2d(smem_u32(smA + stage * A_BYTES), &tmA, fb, kb * bk_elems, mb * BM);
-                    tma_load_2d(smem_u32(smB + stage * B_BYTES), &tmB, fb, kb * bk_elems, nb * BN);
-                    if (++stage == STAGES) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
+                    tma_load_2d(sa + stage * A_BYTES, &tmA, fb, kb * bk_elems, row_a);
+                    tma_load_2d(sb + stage * B_BYTES, &tmB, fb, kb * bk_elems, row_b);
+                }
+                __syncwarp();
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
                 }
             }
         }
-        __syncwarp();
-    } else if (warp == 1) {
-        if (lane == 0) {  // ---------------- MMA issuer
-            int stage = 0;
-            uint32_t phase = 0, acc = 0, acc_phase = 0;
-            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-                mbar_wait(smem_u32(&tempty[acc]), acc_phase ^ 1);
+    } else if (warp == 1) {  // ---------------- MMA issuer (whole warp loops, one lane issues)
+        int stage = 0;
+        uint32_t phase = 0, acc = 0, acc_phase = 0;
+        // descriptors of stage 0; stage s adds s*STAGE/16 to the start-address field
+        const uint64_t ad0 = desc_kmajor_sw128(smem_u32(smA)), bd0 = desc_kmajor_sw128(smem_u32(smB));
+        const uint32_t fb0 = smem_u32(&full[0]), eb0 = smem_u32(&empty[0]);
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            mbar_wait(smem_u32(&tempty[acc]), acc_phase ^ 1);
+            tc_fence_after();
+            const uint32_t d = tmem_base + acc * BN;
+            for (int kb = 0; kb < kblocks; ++kb) {
+                mbar_wait(fb0 + 8 * stage, phase);
                 tc_fence_after();
-                const uint32_t d = tmem_base + acc * BN;
-                for (int kb = 0; kb < kblocks; ++kb) {
-                    mbar_wait(smem_u32(&full[stage]), phase);
-                    tc_fence_after();
-                    const uint64_t ad = desc_kmajor_sw128(smem_u32(smA + stage * A_BYTES));
-                    const uint64_t bd = desc_kmajor_sw128(smem_u32(smB + stage * B_BYTES));
+                if (elect_one()) {
+                    const uint64_t ad = ad0 + static_cast<uint64_t>(stage * (A_BYTES >> 4));
+                    const uint64_t bd = bd0 + static_cast<uint64_t>(stage * (B_BYTES >> 4));
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {  // 4 x 32 bytes of K per stage
                         const uint32_t acc_flag = (kb | k) != 0;
@@ -192,18 +204,18 @@ __global__ void __launch_bounds__(CORE_THREADS + 32 * RNG_WARPS, 1)
                         else
                             mma_f16_ss(d, ad + 2 * k, bd + 2 * k, IDESC, acc_flag);
                     }
-                    tc_commit(smem_u32(&empty[stage]));
-                    if (++stage == STAGES) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
+                    tc_commit(eb0 + 8 * stage);
+                    if (kb == kblocks - 1) tc_commit(smem_u32(&tfull[acc]));
                 }
-                tc_commit(smem_u32(&tfull[acc]));
-                acc ^= 1;
-                if (acc == 0) acc_phase ^= 1;
+                __syncwarp();
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
             }
+            acc ^= 1;
+            if (acc == 0) acc_phase ^= 1;
         }
-        __syncwarp();
     } else if (warp < CORE_THREADS / 32) {  // ---------------- epilogue warps 2..5
         const uint32_t q = hw_warp & 3;  // TMEM lane quarter = physical warp id % 4
         const int row_in_tile = q * 32 + lane;

@@ -20,6 +20,16 @@ __device__ __forceinline__ uint32_t warp_id() {
     return __shfl_sync(0xffffffffu, threadIdx.x / 32, 0);  // warp-uniform
 }
 
+// One lane of a fully active warp (elect.sync): lets the whole warp run a
+// control loop with warp-uniform values while a single thread issues.
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n\t.reg .b32 r;\n\t.reg .pred p;\n\telect.sync r|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(pred));
+    return pred != 0;
+}
+
 // ------------------------------------------------------------------ mbarrier
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
