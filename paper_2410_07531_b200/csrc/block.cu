@@ -161,19 +161,24 @@ static cudaError_t enqueue_step(Block& b, int* launches) {
     GemmJob g;
     g = gemm(c, M, d, d, x.attn_o8, x.wo, x.y1, rgo_gk::EPI_NONE, rgo_gk::OUT_E4M3, c.a_proj, c.s_proj);
     g.rng = rq;
+    const int rw = static_cast<int>(c.rng_block);  // IN_GEMM: RNG warps per GEMM CTA (0 = default)
+    g.rng_warps = rw;
     if ((e = launch_gemm(g, s)) != cudaSuccess) return e;
     ++n;
     g = gemm(c, M, n1, d, x.y1, x.w1, x.h, c.gated ? rgo_gk::EPI_SWIGLU : rgo_gk::EPI_GELU, rgo_gk::OUT_E4M3,
              c.a_ffn1, c.s_ffn1);
     g.rng = rq;
+    g.rng_warps = rw;
     if ((e = launch_gemm(g, s)) != cudaSuccess) return e;
     ++n;
     g = gemm(c, M, d, F, x.h, x.w2, x.x, rgo_gk::EPI_NONE, rgo_gk::OUT_E4M3, c.a_ffn2, c.s_ffn2);
     g.rng = rq;
+    g.rng_warps = rw;
     if ((e = launch_gemm(g, s)) != cudaSuccess) return e;
     ++n;
     g = gemm(c, M, 3 * d, d, x.x, x.wqkv, x.qkv, rgo_gk::EPI_NONE, rgo_gk::OUT_BF16, c.a_qkv, 1.0f);
     g.rng = rq;
+    g.rng_warps = rw;
     if ((e = launch_gemm(g, s)) != cudaSuccess) return e;
     ++n;
     if ((e = record_timing(b, 1, s)) != cudaSuccess) return e;

@@ -7,7 +7,7 @@
 namespace rgo_gk {
 enum { EPI_NONE = 0, EPI_SWIGLU = 1, EPI_GELU = 2 };
 enum { OUT_BF16 = 0, OUT_E4M3 = 1 };
-constexpr int RNG_WARPS_IN_GEMM = 4;  // co-resident RNG warps per GEMM CTA (mechanism B)
+constexpr int RNG_WARPS_IN_GEMM = 4;  // default co-resident RNG warps per GEMM CTA (mechanism B)
 }  // namespace rgo_gk
 
 namespace rgo {
@@ -41,6 +41,7 @@ struct GemmJob {
     float out_scale;         // pre-cast multiplier (fp8 output quantisation)
     int grid;                // 0 = #SMs (persistent)
     const RngQueue* rng;     // non-null: co-resident RNG warps drain this queue
+    int rng_warps;           // 2, 4 or 6 (0 = RNG_WARPS_IN_GEMM)
 };
 
 cudaError_t launch_gemm(const GemmJob& j, cudaStream_t s);

@@ -338,10 +338,14 @@ cudaError_t launch_gemm(const GemmJob& j, cudaStream_t s) {
     int grid = j.grid > 0 ? j.grid : num_sms();
     if (grid > tiles) grid = tiles;
     const bool rng = j.rng != nullptr;
-#define RGO_G(F, E, O)                                                         \
-    if (fp8 == F && j.epi == E && j.out == O)                                  \
-        return rng ? launch_t<F, E, O, RNG_WARPS_IN_GEMM>(ta, tb, p, grid, s)  \
-                   : launch_t<F, E, O, 0>(ta, tb, p, grid, s);
+    const int rw = j.rng_warps ? j.rng_warps : RNG_WARPS_IN_GEMM;
+#define RGO_G(F, E, O)                                                                  \
+    if (fp8 == F && j.epi == E && j.out == O) {                                         \
+        if (!rng) return launch_t<F, E, O, 0>(ta, tb, p, grid, s);                       \
+        if (rw == 2) return launch_t<F, E, O, 2>(ta, tb, p, grid, s);                    \
+        if (rw == 6) return launch_t<F, E, O, 6>(ta, tb, p, grid, s);                    \
+        return launch_t<F, E, O, 4>(ta, tb, p, grid, s);                                 \
+    }
     RGO_G(true, EPI_NONE, OUT_BF16)
     RGO_G(true, EPI_NONE, OUT_E4M3)
     RGO_G(true, EPI_SWIGLU, OUT_E4M3)

@@ -29,7 +29,7 @@ def run(mode, launch=(0, 0, 0), steps=10):
 
 run("no_rng")
 run("serial_fused")
-run("in_gemm")
-for launch in [(0, 0, 0), (148, 128, 0), (148, 256, 0), (148, 384, 0), (296, 128, 0), (296, 256, 0), (444, 128, 0),
-               (74, 256, 0)]:
+for w in (2, 4, 6):
+    run("in_gemm", (0, w, 0))
+for launch in [(148, 128, 0), (148, 256, 0), (296, 128, 0), (296, 256, 0), (444, 256, 0), (74, 256, 0)]:
     run("streams", launch)
