@@ -344,6 +344,7 @@ cudaError_t launch_gemm(const GemmJob& j, cudaStream_t s) {
         if (!rng) return launch_t<F, E, O, 0>(ta, tb, p, grid, s);                       \
         if (rw == 2) return launch_t<F, E, O, 2>(ta, tb, p, grid, s);                    \
         if (rw == 6) return launch_t<F, E, O, 6>(ta, tb, p, grid, s);                    \
+        if (rw == 8) return launch_t<F, E, O, 8>(ta, tb, p, grid, s);                    \
         return launch_t<F, E, O, 4>(ta, tb, p, grid, s);                                 \
     }
     RGO_G(true, EPI_NONE, OUT_BF16)
