@@ -7,7 +7,7 @@
 namespace rgo_gk {
 enum { EPI_NONE = 0, EPI_SWIGLU = 1, EPI_GELU = 2 };
 enum { OUT_BF16 = 0, OUT_E4M3 = 1 };
-constexpr int RNG_WARPS_IN_GEMM = 4;  // default co-resident RNG warps per GEMM CTA (mechanism B)
+constexpr int RNG_WARPS_IN_GEMM = 6;  // default co-resident RNG warps per GEMM CTA (mechanism B)
 }  // namespace rgo_gk
 
 namespace rgo {
