@@ -1,15 +1,23 @@
 #!/bin/bash
-# Capture the round's ncu evidence on ONE GPU (run under gpurun):
+# Capture the round's ncu evidence on ONE GPU (run under gpurun).  Reports are
+# reduced to CSV on the box (raw metrics + per-instruction source page) so the
+# returned gpurun_out/ stays small:
 #   launch list of a short bench run (per-launch device times, serialised)
 #   --set full of each hot kernel: mask (K1), GEMM FP8 (K2), GEMM + RNG warps (K4),
 #   attention with mask bits (K5), attention with inline Philox (K6)
 set -u
 OUT=${1:-gpurun_out}
+KEEP=${KEEP_REPORTS:-""}
 mkdir -p $OUT
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_block.csv \
     python bench.py --steps 2 --warmup 1 --no-cpu-baseline > $OUT/bench_under_ncu.log 2>&1
 for k in mask gemm gemm_rng attn_bits attn_philox; do
     timeout 400 ncu --set full --clock-control none --import-source on -k regex:"gemm_kernel|attn_fwd|rng_mask_kernel" \
-        -s 1 -c 1 -o $OUT/prof_$k python scripts/prof_kernels.py $k > $OUT/ncu_$k.log 2>&1
+        -s 1 -c 1 -o /tmp/prof_$k python scripts/prof_kernels.py $k > $OUT/ncu_$k.log 2>&1
+    ncu -i /tmp/prof_$k.ncu-rep --page raw --csv > $OUT/raw_$k.csv 2>/dev/null
+    ncu -i /tmp/prof_$k.ncu-rep --page source --csv --print-source sass > $OUT/source_$k.csv 2>/dev/null
+    gzip -f $OUT/source_$k.csv
+    if [ -n "$KEEP" ]; then cp /tmp/prof_$k.ncu-rep $OUT/; fi
     tail -1 $OUT/ncu_$k.log
 done
+du -sh $OUT
