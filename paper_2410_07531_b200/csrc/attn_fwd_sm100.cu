@@ -43,7 +43,9 @@ using namespace sm100;
 constexpr int BQ = 128;  // rows per Q tile (one softmax warpgroup)
 constexpr int BKV = 128;
 constexpr int KV_STAGES = 2;
-constexpr int THREADS = 320;
+constexpr int THREADS = 384;        // 3 warpgroups: control, softmax tile 0, softmax tile 1
+constexpr int CTRL_REGS = 56;       // setmaxnreg budget of the control warpgroup
+constexpr int SOFTMAX_REGS = 224;   // ... and of each softmax warpgroup (4*56 + 8*224 = 65536/32)
 constexpr uint32_t TMEM_COLS = 512;
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
 
@@ -186,62 +188,73 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(const __grid_const
     const uint32_t tmem = *tmem_slot;
     constexpr int NCH = HD / 64;
 
-    if (warp == 0) {
-        if (lane == 0) {  // ------------------------------------------------ TMA
+    if (warp < 4) {  // ---------------------------------------------- control warpgroup
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(CTRL_REGS));
+        if (warp == 0) {  // TMA producer (whole warp loops, one lane issues)
             const uint32_t qb = smem_u32(q_full);
-            mbar_arrive_expect_tx(qb, 2 * SM::TILE);
-            for (int w = 0; w < 2; ++w)
-                for (int c = 0; c < NCH; ++c)
-                    tma_load_4d(smem_u32(sQ + w * SM::TILE + c * SM::CHUNK), &tmQ, qb, c * 64, q0 + w * BQ, hh, bb);
+            if (elect_one()) {
+                mbar_arrive_expect_tx(qb, 2 * SM::TILE);
+                for (int w = 0; w < 2; ++w)
+                    for (int c = 0; c < NCH; ++c)
+                        tma_load_4d(smem_u32(sQ + w * SM::TILE + c * SM::CHUNK), &tmQ, qb, c * 64, q0 + w * BQ, hh, bb);
+            }
+            __syncwarp();
             int ks = 0, vs = 0;
             uint32_t kph = 0, vph = 0;
             for (int j = 0; j < n_kv; ++j) {
                 mbar_wait(smem_u32(&k_empty[ks]), kph ^ 1);
-                const uint32_t kb = smem_u32(&k_full[ks]);
-                mbar_arrive_expect_tx(kb, SM::TILE);
-                for (int c = 0; c < NCH; ++c)
-                    tma_load_4d(smem_u32(sK + ks * SM::TILE + c * SM::CHUNK), &tmK, kb, c * 64, j * BKV, hh, bb);
+                if (elect_one()) {
+                    const uint32_t kb = smem_u32(&k_full[ks]);
+                    mbar_arrive_expect_tx(kb, SM::TILE);
+                    for (int c = 0; c < NCH; ++c)
+                        tma_load_4d(smem_u32(sK + ks * SM::TILE + c * SM::CHUNK), &tmK, kb, c * 64, j * BKV, hh, bb);
+                }
+                __syncwarp();
                 if (++ks == KV_STAGES) { ks = 0; kph ^= 1; }
                 mbar_wait(smem_u32(&v_empty[vs]), vph ^ 1);
-                const uint32_t vb = smem_u32(&v_full[vs]);
-                mbar_arrive_expect_tx(vb, SM::TILE);
-                for (int c = 0; c < NCH; ++c)
-                    tma_load_4d(smem_u32(sV + vs * SM::TILE + c * SM::CHUNK), &tmV, vb, c * 64, j * BKV, hh, bb);
+                if (elect_one()) {
+                    const uint32_t vb = smem_u32(&v_full[vs]);
+                    mbar_arrive_expect_tx(vb, SM::TILE);
+                    for (int c = 0; c < NCH; ++c)
+                        tma_load_4d(smem_u32(sV + vs * SM::TILE + c * SM::CHUNK), &tmV, vb, c * 64, j * BKV, hh, bb);
+                }
+                __syncwarp();
                 if (++vs == KV_STAGES) { vs = 0; vph ^= 1; }
             }
-        }
-        __syncwarp();
-    } else if (warp == 1) {
-        if (lane == 0) {  // ------------------------------------------------ MMA
+        } else if (warp == 1) {  // MMA issuer (whole warp loops, one lane issues)
             constexpr uint32_t IDESC_S = idesc_make(1, 1, BQ, BKV, 0, 0);
             constexpr uint32_t IDESC_O = idesc_make(1, 1, BQ, HD, 0, 1);  // V is MN-major
+            const uint64_t q_desc = desc_kmajor_sw128(smem_u32(sQ));
+            const uint64_t k_desc = desc_kmajor_sw128(smem_u32(sK));
+            // V: MN-major SW128, 8-key groups at 1024 B (SBO), 64-dH chunks at CHUNK (LBO)
+            const uint64_t v_desc = desc_sw128(smem_u32(sV), SM::CHUNK, 1024);
             auto issue_s = [&](int w, int ks) {
 #pragma unroll
                 for (int kk = 0; kk < HD / 16; ++kk) {
-                    const uint32_t off = (kk >> 2) * SM::CHUNK + (kk & 3) * 32;
-                    const uint64_t a = desc_kmajor_sw128(smem_u32(sQ + w * SM::TILE + off));
-                    const uint64_t b = desc_kmajor_sw128(smem_u32(sK + ks * SM::TILE + off));
-                    mma_f16_ss(tmem + w * 128, a, b, IDESC_S, kk > 0);
+                    const uint32_t off = ((kk >> 2) * SM::CHUNK + (kk & 3) * 32) >> 4;
+                    mma_f16_ss(tmem + w * 128, q_desc + ((w * SM::TILE) >> 4) + off,
+                               k_desc + ((ks * SM::TILE) >> 4) + off, IDESC_S, kk > 0);
                 }
             };
             auto issue_o = [&](int w, int vs, bool acc) {
 #pragma unroll
-                for (int kk = 0; kk < BKV / 16; ++kk) {
-                    // V: MN-major SW128, 8-key groups at 1024 B (SBO), 64-dH chunks at CHUNK (LBO)
-                    const uint64_t b = desc_sw128(smem_u32(sV + vs * SM::TILE + kk * 2048), SM::CHUNK, 1024);
-                    mma_f16_ts(tmem + 256 + w * 128, tmem + w * 128 + kk * 8, b, IDESC_O, (acc || kk > 0) ? 1u : 0u);
-                }
+                for (int kk = 0; kk < BKV / 16; ++kk)
+                    mma_f16_ts(tmem + 256 + w * 128, tmem + w * 128 + kk * 8,
+                               v_desc + ((vs * SM::TILE + kk * 2048) >> 4), IDESC_O, (acc || kk > 0) ? 1u : 0u);
             };
             mbar_wait(smem_u32(q_full), 0);
             int ks = 0, vs = 0;
             uint32_t kph = 0, vph = 0;
             mbar_wait(smem_u32(&k_full[ks]), kph);
             tc_fence_after();
-            issue_s(0, ks);
-            tc_commit(smem_u32(&s_full[0]));
-            issue_s(1, ks);
-            tc_commit(smem_u32(&s_full[1]));
-            tc_commit(smem_u32(&k_empty[ks]));
+            if (elect_one()) {
+                issue_s(0, ks);
+                tc_commit(smem_u32(&s_full[0]));
+                issue_s(1, ks);
+                tc_commit(smem_u32(&s_full[1]));
+                tc_commit(smem_u32(&k_empty[ks]));
+            }
+            __syncwarp();
             if (++ks == KV_STAGES) { ks = 0; kph ^= 1; }
             for (int j = 0; j < n_kv; ++j) {
                 const bool has_next = j + 1 < n_kv;
@@ -251,25 +264,30 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(const __grid_const
                 for (int w = 0; w < 2; ++w) {
                     mbar_wait(smem_u32(&p_full[w]), j & 1);
                     tc_fence_after();
-                    issue_o(w, vs, j > 0);
-                    if (has_next) {
-                        issue_s(w, ks);
-                        tc_commit(smem_u32(&s_full[w]));
+                    if (elect_one()) {
+                        issue_o(w, vs, j > 0);
+                        if (has_next) {
+                            issue_s(w, ks);
+                            tc_commit(smem_u32(&s_full[w]));
+                        }
+                        if (w == 1) {
+                            tc_commit(smem_u32(&v_empty[vs]));
+                            if (has_next) tc_commit(smem_u32(&k_empty[ks]));
+                            if (!has_next) {
+                                tc_commit(smem_u32(&o_done[0]));
+                                tc_commit(smem_u32(&o_done[1]));
+                            }
+                        }
                     }
+                    __syncwarp();
                 }
-                tc_commit(smem_u32(&v_empty[vs]));
                 if (++vs == KV_STAGES) { vs = 0; vph ^= 1; }
-                if (has_next) {
-                    tc_commit(smem_u32(&k_empty[ks]));
-                    if (++ks == KV_STAGES) { ks = 0; kph ^= 1; }
-                }
+                if (has_next && ++ks == KV_STAGES) { ks = 0; kph ^= 1; }
             }
-            tc_commit(smem_u32(&o_done[0]));
-            tc_commit(smem_u32(&o_done[1]));
         }
-        __syncwarp();
     } else {  // -------------------------------------------------------- softmax
-        const int w = (warp - 2) >> 2;
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(SOFTMAX_REGS));
+        const int w = (warp - 4) >> 2;
         const uint32_t q = warp & 3;
         const int row = q * 32 + lane;
         const int i = q0 + w * BQ + row;  // query index within the slice
@@ -280,13 +298,22 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(const __grid_const
         const uint64_t slice = static_cast<uint64_t>(bb) * p.H + hh;
         const uint64_t row_base = (slice * p.S + static_cast<uint64_t>(row_valid ? i : 0)) * p.S;
         float m = -INFINITY, l = 0.0f;
+        // MASK_BITS: the 16 bytes of tile j+1 are loaded while tile j is processed
+        uint32_t kw_next[4] = {0u, 0u, 0u, 0u};
+        if (MODE == MASK_BITS && row_valid) keep_bits<MODE, R>(p, row_base, kw_next);
         for (int j = 0; j < n_kv; ++j) {
             const int j0 = j * BKV;
             uint32_t kw[4];
-            if (row_valid)
-                keep_bits<MODE, R>(p, row_base + j0, kw);
-            else
+            if constexpr (MODE == MASK_BITS) {
                 kw[0] = kw[1] = kw[2] = kw[3] = 0;
+#pragma unroll
+                for (int t = 0; t < 4; ++t) kw[t] = kw_next[t];
+                if (row_valid && j + 1 < n_kv) keep_bits<MODE, R>(p, row_base + j0 + BKV, kw_next);
+            } else if (row_valid) {
+                keep_bits<MODE, R>(p, row_base + j0, kw);
+            } else {
+                kw[0] = kw[1] = kw[2] = kw[3] = 0;
+            }
             mbar_wait(smem_u32(&s_full[w]), j & 1);
             tc_fence_after();
             uint32_t s[4][32];
