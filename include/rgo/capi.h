@@ -108,7 +108,7 @@ int rgo_uniform_fill(uint64_t seed, uint32_t stream_id, uint64_t n, void* d_bf16
 
 /* Dropout-mask work queue (overlap mechanism B tail / dynamic scheduling):
  * drains vectors [*d_counter, n/128) of layout d into d_bits, claiming
- * 32-vector chunks with atomics on d_counter (zero it before the first
+ * 64-vector chunks with atomics on d_counter (zero it before the first
  * producer of a pass).  Requires B*nH*SQ^2 % 128 == 0 and threshold < 2^32. */
 int rgo_mask_queue_drain(const rgo_mask_desc* d, uint8_t* d_bits, uint64_t bytes,
                          unsigned long long* d_counter, const rgo_launch* launch,

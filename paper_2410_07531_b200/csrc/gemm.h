@@ -15,7 +15,7 @@ namespace rgo {
 // Dropout-mask work queue shared by the GEMM-resident RNG warps and the
 // tail/stand-alone queue kernel.  Unit = one 16-byte vector (128 elements);
 // *counter (device, zeroed before the first producer) hands out chunks of
-// 32 vectors (one per lane of the claiming warp).
+// 64 vectors (two per lane of the claiming warp).
 struct RngQueue {
     uint8_t* out;            // packed mask, 16-byte aligned
     uint64_t n_vec;          // elems / 128 (elems % 128 == 0 required)

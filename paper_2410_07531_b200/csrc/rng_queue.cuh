@@ -1,5 +1,5 @@
 // rng_queue.cuh -- dropout-mask work queue (overlap mechanism B).
-// Warps claim 32-vector chunks (one 128-element vector per lane) from a
+// Warps claim 64-vector chunks (two 128-element vectors per lane) from a
 // global counter; the same device routine runs inside the GEMM CTAs
 // (co-resident RNG warps, until the GEMM's epilogue warps finish) and in the
 // tail kernel that drains whatever the GEMMs left.  Bits are identical to K1:
@@ -34,6 +34,32 @@ __device__ __forceinline__ void rng_vector(const RngQueue& q, uint64_t v, uint32
                  : "memory");
 }
 
+// Two vectors at once (independent counters -> interleavable chains).
+template <int R>
+__device__ __forceinline__ void rng_vector2(const RngQueue& q, uint64_t va, uint64_t vb, uint32_t k0, uint32_t k1,
+                                            uint32_t thr) {
+    const uint64_t ca = q.base_offset + va * 32, cb = q.base_offset + vb * 32;
+    const uint32_t la = static_cast<uint32_t>(ca), lb = static_cast<uint32_t>(cb);
+    if (la > 0xFFFFFFFFu - 31u || lb > 0xFFFFFFFFu - 31u) {  // rare: a unit straddles a 2^32 counter boundary
+        rng_vector<R>(q, va, k0, k1, thr);
+        rng_vector<R>(q, vb, k0, k1, thr);
+        return;
+    }
+    const uint32_t ha = static_cast<uint32_t>(ca >> 32), hb = static_cast<uint32_t>(cb >> 32);
+    uint32_t wa[4], wb[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        wa[t] = rgo_dev::keep32_nowrap<R>(la + 8 * t, ha, k0, k1, thr, 0u);
+        wb[t] = rgo_dev::keep32_nowrap<R>(lb + 8 * t, hb, k0, k1, thr, 0u);
+    }
+    uint8_t* pa = q.out + va * 16;
+    uint8_t* pb = q.out + vb * 16;
+    asm volatile("st.global.cs.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(pa), "r"(wa[0]), "r"(wa[1]), "r"(wa[2]), "r"(wa[3])
+                 : "memory");
+    asm volatile("st.global.cs.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(pb), "r"(wb[0]), "r"(wb[1]), "r"(wb[2]), "r"(wb[3])
+                 : "memory");
+}
+
 // Drain until the queue is empty or (*stop >= stop_at) is observed.
 template <int R>
 __device__ __forceinline__ void rng_drain_r(const RngQueue& q, const volatile int* stop, int stop_at) {
@@ -46,12 +72,18 @@ __device__ __forceinline__ void rng_drain_r(const RngQueue& q, const volatile in
     asm volatile("" : "+r"(k0), "+r"(k1), "+r"(thr) : "r"(lane));
     while (true) {
         if (stop && *stop >= stop_at) break;
+        // 64 vectors per claim, two per lane: 16 independent Philox chains
+        // per thread keep the fma-heavy pipe fed with few warps
         unsigned long long start = 0;
-        if (lane == 0) start = atomicAdd(q.counter, 32ull);
+        if (lane == 0) start = atomicAdd(q.counter, 64ull);
         start = __shfl_sync(0xffffffffu, start, 0);
         if (start >= q.n_vec) break;
-        const uint64_t v = start + lane;
-        if (v < q.n_vec) rng_vector<R>(q, v, k0, k1, thr);
+        const uint64_t v0 = start + lane, v1 = start + 32 + lane;
+        if (v1 < q.n_vec) {
+            rng_vector2<R>(q, v0, v1, k0, k1, thr);
+        } else {
+            if (v0 < q.n_vec) rng_vector<R>(q, v0, k0, k1, thr);
+        }
     }
 }
 

@@ -29,7 +29,7 @@ def run(mode, launch=(0, 0, 0), steps=10):
 
 run("no_rng")
 run("serial_fused")
-for w in (6, 8):
+for w in (4, 6, 8):
     run("in_gemm", (0, w, 0))
 for launch in [(148, 128, 0)]:
     run("streams", launch)
