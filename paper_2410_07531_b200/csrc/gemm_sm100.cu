@@ -342,7 +342,6 @@ cudaError_t launch_gemm(const GemmJob& j, cudaStream_t s) {
 #define RGO_G(F, E, O)                                                                  \
     if (fp8 == F && j.epi == E && j.out == O) {                                         \
         if (!rng) return launch_t<F, E, O, 0>(ta, tb, p, grid, s);                       \
-        if (rw == 2) return launch_t<F, E, O, 2>(ta, tb, p, grid, s);                    \
         if (rw == 6) return launch_t<F, E, O, 6>(ta, tb, p, grid, s);                    \
         if (rw == 8) return launch_t<F, E, O, 8>(ta, tb, p, grid, s);                    \
         return launch_t<F, E, O, 4>(ta, tb, p, grid, s);                                 \
