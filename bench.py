@@ -106,13 +106,8 @@ def barrier(world):
 
 
 def max_over_ranks(x: float, world: int) -> float:
-    if world == 1:
-        return x
-    import torch
-    import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    from paper_2410_07531_b200.sharding import max_over_ranks as mor
+    return x if world == 1 else mor(x)
 
 
 # --------------------------------------------------------------------- CPU side
@@ -195,7 +190,8 @@ def bench_mask_kernel(rgo, cfg, rank, steps, warmup):
     import torch
     B, H, S = cfg["batch"], cfg["heads"], cfg["seq"]
     elems = B * H * S * S
-    lay = rgo.MaskLayout(B, H, S, 42, rank * elems // 4)
+    from paper_2410_07531_b200.sharding import replica_base_offset
+    lay = rgo.MaskLayout(B, H, S, 42, replica_base_offset(B, H, S, rank))
     thr = rgo.KeepThreshold(cfg["keep_prob"])
     out = torch.empty(elems // 8, dtype=torch.uint8, device="cuda")
     for _ in range(warmup):
@@ -212,7 +208,8 @@ def bench_block(args, rank, world):
     wl = rgo.WorkloadConfig(batch=cfg["batch"], seq=cfg["seq"], heads=cfg["heads"], head_dim=cfg["head_dim"],
                             ffn_dim=cfg["ffn"], gated=True, keep_prob=cfg["keep_prob"], philox_rounds=cfg["rounds"])
     elems = cfg["batch"] * cfg["heads"] * cfg["seq"] ** 2
-    base = rank * elems // 4  # disjoint Philox counter range per rank
+    from paper_2410_07531_b200.sharding import replica_base_offset
+    base = replica_base_offset(cfg["batch"], cfg["heads"], cfg["seq"], rank)  # disjoint Philox counters per rank
     weights = rgo.block.make_weights(wl, 42, torch.device("cuda"))
     modes = ["serial_fused", "streams", "in_gemm", "no_rng"]
     launch = {"streams": tuple(args.rng_launch), "in_gemm": (0, args.rng_warps, 0)}

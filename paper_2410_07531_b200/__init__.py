@@ -13,6 +13,7 @@ from .mask import (DropoutMask, KeepThreshold, MaskLayout, element_source, gener
 from .ref_attention import (AttentionInput, AttentionOutput, EquivCase, EquivResult, attention_dropout_decoupled,
                             attention_dropout_fused, attention_forward, attn_fwd, default_equiv_grid,
                             random_attention_input, run_equiv_suite)
+from . import sharding
 from .block import Block
 from .gemm import (GemmShape, WorkloadConfig, attention_work, gemm, gemm_shapes, gemm_with_rng,
                    mask_queue_drain, rng_elements, workload_preset)
