@@ -186,6 +186,24 @@ int rgo_attn_fwd(const rgo_attn_desc* a, const rgo_tensor4* q, const rgo_tensor4
                  const rgo_tensor4* v, const uint8_t* d_bits, uint64_t bits_bytes,
                  const rgo_tensor4* o, float* d_lse, rgo_stream_t stream);
 
+/* K7: flash-attention backward with dropout -- the training counterpart of
+ * rgo_attn_fwd (the reference stops at the forward: ref_attention.hpp:56-92,
+ * SPEC.md:552).  Exact derivative of the forward's semantics: with
+ * P = softmax(scale Q K^T), W = keep ? P/p : 0, O = W V,
+ *   dV = W^T dO,  dP = keep ? dO V^T / p : 0,  dS = P o (dP - rowsum(dO o O)),
+ *   dQ = scale dS K,  dK = scale dS^T Q.
+ * a, q, k, v, d_bits as for the forward (same mask source, seed, offset and
+ * rounds, so the keep bits are the forward's); o and d_lse are the forward's
+ * output and LSE; d_o the incoming gradient; dq/dk/dv receive bf16 gradients
+ * (same view convention).  d_work: device scratch of
+ * rgo_attn_bwd_workspace() bytes (fp32 dQ accumulator + per-row terms). */
+int rgo_attn_bwd_workspace(const rgo_attn_desc* a, uint64_t* bytes);
+int rgo_attn_bwd(const rgo_attn_desc* a, const rgo_tensor4* q, const rgo_tensor4* k,
+                 const rgo_tensor4* v, const rgo_tensor4* o, const rgo_tensor4* d_o,
+                 const float* d_lse, const uint8_t* d_bits, uint64_t bits_bytes,
+                 const rgo_tensor4* dq, const rgo_tensor4* dk, const rgo_tensor4* dv,
+                 void* d_work, uint64_t work_bytes, rgo_stream_t stream);
+
 /* ------------------------------------------------------ host-buffer entry --
  * Drop-in forms of the reference's value-semantics API: host arrays in and
  * out, the library stages them through device memory it allocates and frees

@@ -147,3 +147,39 @@ def attention(q, k, v, slices, seq, head_dim, mode=0, seed=0, base_offset=0, p=1
 def fnv1a64(data: np.ndarray) -> int:
     data = np.ascontiguousarray(data, np.uint8)
     return int(lib().oracle_fnv1a64(data, data.size))
+
+
+# ---------------------------------------------------------------- backward
+def unpack_keep(bits, slices, seq):
+    """Packed LSB-first mask (mask.hpp:183-186, 291-295) -> bool [slices, seq, seq]."""
+    n = slices * seq * seq
+    return np.unpackbits(np.ascontiguousarray(bits, np.uint8), bitorder="little")[:n].astype(bool).reshape(
+        slices, seq, seq)
+
+
+def attention_backward(q, k, v, do, slices, seq, head_dim, keep=None, p=1.0):
+    """Analytic gradient of the reference forward (ref_attention.hpp:56-92) in
+    float64.  The reference has no backward: this restates the
+    derivative of forward_impl's semantics -- softmax over ALL keys before
+    dropout (:78-82), kept weights scaled by 1/float(p) (:84-85, :125) -- and
+    is cross-checked against torch float64 autograd in tests/test_oracle.py.
+    q, k, v, do: arrays of slices*seq*head_dim; keep: bool [slices, seq, seq]
+    or None (no dropout).  Returns (o, dq, dk, dv), each [slices, seq, head_dim]."""
+    sh = (slices, seq, head_dim)
+    q, k, v, do = (np.asarray(x, np.float64).reshape(sh) for x in (q, k, v, do))
+    scale = float(np.float32(1.0) / np.sqrt(np.float32(head_dim)))
+    pf = float(np.float32(p))
+    s = scale * np.einsum("sid,sjd->sij", q, k)
+    s -= s.max(axis=-1, keepdims=True)
+    e = np.exp(s)
+    P = e / e.sum(axis=-1, keepdims=True)
+    km = np.ones_like(P) if keep is None else keep.astype(np.float64)
+    W = km * P / pf
+    o = np.einsum("sij,sjd->sid", W, v)
+    dv = np.einsum("sij,sid->sjd", W, do)
+    dP = km * np.einsum("sid,sjd->sij", do, v) / pf
+    D = (P * dP).sum(axis=-1, keepdims=True)
+    dS = P * (dP - D)
+    dq = scale * np.einsum("sij,sjd->sid", dS, k)
+    dk = scale * np.einsum("sij,sid->sjd", dS, q)
+    return o, dq, dk, dv

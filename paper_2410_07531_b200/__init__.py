@@ -11,7 +11,7 @@ from .mask import (DropoutMask, KeepThreshold, MaskLayout, element_source, gener
                    generate_mask_device, keep_bit_direct, load_mask, mask_bit, save_mask)
 
 from .ref_attention import (AttentionInput, AttentionOutput, EquivCase, EquivResult, attention_dropout_decoupled,
-                            attention_dropout_fused, attention_forward, attn_fwd, default_equiv_grid,
+                            attention_dropout_fused, attention_forward, attn_bwd, attn_fwd, DropoutAttention, default_equiv_grid,
                             random_attention_input, run_equiv_suite)
 from . import sharding
 from .block import Block
@@ -21,7 +21,7 @@ from .gemm import (GemmShape, WorkloadConfig, attention_work, gemm, gemm_shapes,
 __all__ = [
     "Block",
     "AttentionInput", "AttentionOutput", "EquivCase", "EquivResult", "attention_dropout_decoupled",
-    "attention_dropout_fused", "attention_forward", "attn_fwd", "default_equiv_grid", "random_attention_input",
+    "attention_dropout_fused", "attention_forward", "attn_bwd", "attn_fwd", "DropoutAttention", "default_equiv_grid", "random_attention_input",
     "run_equiv_suite",
     "GemmShape", "WorkloadConfig", "attention_work", "gemm", "gemm_shapes", "gemm_with_rng",
     "mask_queue_drain", "rng_elements", "workload_preset",

@@ -122,6 +122,12 @@ SIGNATURES = {
         [C.POINTER(attn_desc), C.POINTER(tensor4), C.POINTER(tensor4), C.POINTER(tensor4), C.c_void_p,
          C.c_uint64, C.POINTER(tensor4), C.c_void_p, C.c_void_p],
     ),
+    "rgo_attn_bwd_workspace": (C.c_int, [C.POINTER(attn_desc), C.POINTER(C.c_uint64)]),
+    "rgo_attn_bwd": (
+        C.c_int,
+        [C.POINTER(attn_desc)] + [C.POINTER(tensor4)] * 5 + [C.c_void_p, C.c_void_p, C.c_uint64]
+        + [C.POINTER(tensor4)] * 3 + [C.c_void_p, C.c_uint64, C.c_void_p],
+    ),
     "rgo_block_create": (C.c_int, [C.POINTER(block_desc), C.POINTER(block_buffers), C.c_int32, C.c_void_p]),
     "rgo_block_step": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "rgo_block_last_timings": (C.c_int, [C.c_void_p, C.c_void_p]),

@@ -56,4 +56,24 @@ struct AttnJob {
 
 cudaError_t launch_attn_fwd(const AttnJob& j, cudaStream_t s);
 
+// K7 backward (attn_bwd_sm100.cu): dQ, dK, dV from Q, K, V, the forward
+// output O, its natural-log LSE and dO; same mask sources as the forward.
+struct AttnBwdJob {
+    int B, H, S, HD;
+    float scale;
+    AttnTensor q, k, v, o, dout;
+    AttnOut dq, dk, dv;
+    const float* lse;        // [B*H*S] from the forward
+    int mode;                // rgo_attn::MASK_*
+    float keep_prob;
+    const uint8_t* bits;
+    uint64_t bits_bytes;
+    uint64_t seed, base_offset, threshold;
+    int rounds;
+    void* work;              // attn_bwd_workspace_bytes()
+};
+
+uint64_t attn_bwd_workspace_bytes(int B, int H, int S, int HD);
+cudaError_t launch_attn_bwd(const AttnBwdJob& j, cudaStream_t s);
+
 }  // namespace rgo

@@ -1,0 +1,721 @@
+// attn_bwd_sm100.cu -- K7: Blackwell flash-attention backward with dropout.
+//
+// The training counterpart of K5/K6 (attn_fwd_sm100.cu).  The reference stops
+// at the forward (ref_attention.hpp:56-92; SPEC.md:552 puts backward out of its
+// scope), so the semantics are the exact derivative of that forward:
+//   P  = softmax(scale * Q K^T) over ALL keys (ref_attention.hpp:78-82)
+//   W  = keep ? P / p : 0                     (:84-85, p = float keep_prob)
+//   O  = W V
+//   dV = W^T dO
+//   dP = keep ? (dO V^T) / p : 0
+//   D  = rowsum(dO o O)            (= rowsum(P o dP))
+//   dS = P o (dP - D)
+//   dQ = scale * dS K,   dK = scale * dS^T Q
+// with the keep bit of (slice s, query i, key j) = element (s*SQ + i)*SQ + j of
+// the reference mask layout (mask.hpp:35-39), read from the bitmask
+// (MASK_BITS, the paper's decoupled path) or regenerated with Philox inline
+// (MASK_PHILOX, the conventional fused baseline; identical keep decisions).
+//
+// Three kernels:
+//   bwd_prep   per query row: D = dO.O, -lse*log2(e) (padding rows: D 0, -inf),
+//              zeroes the fp32 dQ accumulator (HBM-bound, small)
+//   bwd_main   one CTA per (slice, 128-key tile); loops over 128-query tiles:
+//                S^T  = K Q^T      (SS, TMEM [0,128))
+//                dP^T = V dO^T     (SS, TMEM [128,256))
+//                dV  += W^T dO     (TS: W^T bf16 from TMEM, dO MN-major)
+//                dK  += dS^T Q     (TS: dS^T bf16 from TMEM, Q MN-major)
+//                dQ_i = dS K       (SS: dS MN-major from smem, K MN-major) -> TMEM [128,..)
+//              keys on TMEM lanes (one thread per key row), so dV/dK
+//              accumulate in TMEM for the whole loop; dQ tiles are reduced
+//              into an fp32 accumulator with coalesced red.global.add.v4.f32.
+//   bwd_dq     dQ = scale * accumulator -> bf16
+//
+// Warp roles of bwd_main (512 threads, 128 registers each):
+//   warp 0      TMA: K, V once; Q (+ its -lse2 / D rows) and dO through 2-stage rings
+//   warp 1      MMA issuer (one elected lane)
+//   warps 4-7   "softmax" WG 0: queries [0,64) of each tile, one thread per key
+//   warps 8-11  softmax WG 1: queries [64,128)
+//   warps 12-15 dQ drain: TMEM -> red.global.add.v4.f32
+// Per query tile i the MMA order is  dP(i), dV(i), S(i+1), dK(i), dQ(i):
+// the softmax's P phase of tile i overlaps dK(i-1)/dQ(i-1)/dP(i), its dS
+// phase overlaps dV(i)/S(i+1).
+// Mask bits arrive row-major (16 B per query row per 128-key tile); with keys
+// on lanes each warp transposes its 32x32 bit blocks with a 5-stage
+// shuffle butterfly.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "attn.h"
+#include "philox.cuh"
+#include "sm100_ptx.cuh"
+#include "tma_host.h"
+
+namespace rgo_attn_bwd {
+
+using namespace sm100;
+using rgo_attn::MASK_BITS;
+using rgo_attn::MASK_NONE;
+using rgo_attn::MASK_PHILOX;
+
+constexpr int BQ = 128;   // queries per tile
+constexpr int BKV = 128;  // keys per CTA
+constexpr int STAGES = 2;
+constexpr int THREADS = 512;
+constexpr uint32_t TMEM_COLS = 512;
+constexpr int MAX_DSMEM = 232448;  // 227 KiB opt-in maximum on sm_100
+
+struct Params {
+    int B, H, S, n_qt, n_kt;
+    float scale;        // softmax scale (dQ, dK)
+    float scale_log2;   // scale * log2(e)
+    float inv_keep;     // 1 / float keep_prob (1 without dropout)
+    const uint8_t* bits;
+    uint64_t bits_bytes;
+    int bits_aligned;   // SQ % 32 == 0 and 4-byte aligned bits: one word per row per warp
+    uint32_t k0, k1;
+    uint64_t base_offset;
+    uint32_t thr;
+    int rounds;
+    const float* rows;  // [slices][n_qt*128][2]: per query tile 128 x -lse*log2e, then 128 x D
+    float* dq_acc;      // blocked fp32 accumulator (see dq_index)
+    void* dK;
+    void* dV;
+    long long k_sb, k_sh, k_ss;  // dK strides (elements)
+    long long v_sb, v_sh, v_ss;  // dV strides
+};
+
+// Blocked dQ accumulator: per (slice, query tile) HD/32 column chunks of 8
+// groups x 128 rows x float4, so the 32 lanes of a drain warp (32 consecutive
+// rows) add 512 contiguous bytes per instruction.
+__host__ __device__ __forceinline__ uint64_t dq_tile_base(uint64_t slice, int n_qt, int qt, int HD) {
+    return (slice * n_qt + qt) * static_cast<uint64_t>(BQ) * HD;
+}
+__host__ __device__ __forceinline__ uint32_t dq_off(int row, int col) {  // within a tile
+    return ((static_cast<uint32_t>(col >> 2) * BQ) + row) * 4 + (col & 3);
+}
+
+template <int HD>
+struct Smem {
+    static constexpr int CHUNK = 128 * 128;         // 128 rows x 128 B (one SW128 column block)
+    static constexpr int TILE = (HD / 64) * CHUNK;  // 128 rows x HD bf16
+    static constexpr int K_OFF = 0;
+    static constexpr int V_OFF = TILE;
+    static constexpr int Q_OFF = 2 * TILE;
+    static constexpr int DO_OFF = Q_OFF + STAGES * TILE;
+    static constexpr int DS_OFF = DO_OFF + STAGES * TILE;  // dS [128 keys][128 queries] bf16
+    static constexpr int ROW_OFF = DS_OFF + 2 * CHUNK;     // per stage: 128 -lse2, 128 D
+    static constexpr int BAR_OFF = ROW_OFF + STAGES * 1024;
+    static constexpr int BYTES = BAR_OFF + 256;
+    static constexpr int ALLOC = (BYTES + 1023 <= MAX_DSMEM) ? BYTES + 1023 : MAX_DSMEM;
+};
+
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+
+__device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
+                 : "memory");
+}
+
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ float bf16_lo(uint32_t v) { return __uint_as_float(v << 16); }
+__device__ __forceinline__ float bf16_hi(uint32_t v) { return __uint_as_float(v & 0xFFFF0000u); }
+
+// 32x32 bit transpose across a warp: in, lane l holds row l (bit c = column
+// c); out, lane l holds column l (bit r = row r's bit l).  Five butterfly
+// stages swap the off-diagonal s x s blocks of lane pairs (l, l^s).
+__device__ __forceinline__ uint32_t transpose32(uint32_t a, uint32_t lane) {
+    const uint32_t lo_masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+    for (int t = 0; t < 5; ++t) {
+        const int s = 16 >> t;
+        const uint32_t lo = lo_masks[t];
+        const uint32_t other = __shfl_xor_sync(0xffffffffu, a, s);
+        const bool top = (lane & s) == 0;
+        const uint32_t x = top ? (other << s) : (other >> s);
+        const uint32_t m = top ? lo : ~lo;
+        a = (a & m) | (x & ~m);
+    }
+    return a;
+}
+
+// Keep bits of 32 consecutive elements of one query row, starting at global
+// element idx0 (bit c = element idx0 + c); elements >= n_valid_cols of the
+// row are cleared.
+template <int MODE, int R>
+__device__ __forceinline__ uint32_t row_word(const Params& p, uint64_t idx0, int n_valid) {
+    if (n_valid <= 0) return 0u;
+    uint32_t w;
+    if constexpr (MODE == MASK_BITS) {
+        if (p.bits_aligned) {
+            w = __ldg(reinterpret_cast<const uint32_t*>(p.bits) + (idx0 >> 5));
+        } else {
+            const uint64_t b0 = idx0 >> 3;
+            const uint32_t sh = static_cast<uint32_t>(idx0 & 7);
+            uint64_t acc = 0;
+#pragma unroll
+            for (int t = 0; t < 5; ++t) {
+                const uint64_t b = b0 + t;
+                acc |= static_cast<uint64_t>(b < p.bits_bytes ? p.bits[b] : 0u) << (8 * t);
+            }
+            w = static_cast<uint32_t>(acc >> sh);
+        }
+    } else if constexpr (MODE == MASK_PHILOX) {
+        if ((idx0 & 3) == 0) {
+            const uint64_t ctr = p.base_offset + (idx0 >> 2);
+            const uint32_t lo = static_cast<uint32_t>(ctr), hi = static_cast<uint32_t>(ctr >> 32);
+            if (R > 0 && lo <= 0xFFFFFFFFu - 7u) {
+                w = rgo_dev::keep32_nowrap<(R > 0 ? R : 1)>(lo, hi, p.k0, p.k1, p.thr, 0u);
+            } else {
+                w = 0;
+#pragma unroll 1
+                for (int b = 0; b < 8; ++b) {
+                    const uint64_t c = ctr + b;
+                    const uint4 o = rgo_dev::philox_rt(static_cast<uint32_t>(c), static_cast<uint32_t>(c >> 32), 0u,
+                                                       0u, p.k0, p.k1, p.rounds);
+                    w |= (static_cast<uint32_t>(o.x < p.thr) | (static_cast<uint32_t>(o.y < p.thr) << 1) |
+                          (static_cast<uint32_t>(o.z < p.thr) << 2) | (static_cast<uint32_t>(o.w < p.thr) << 3))
+                         << (4 * b);
+                }
+            }
+        } else {
+            w = 0;
+#pragma unroll 1
+            for (int c = 0; c < 32; ++c) {
+                const uint64_t idx = idx0 + c;
+                const uint64_t ctr = p.base_offset + (idx >> 2);
+                const uint4 o = rgo_dev::philox_rt(static_cast<uint32_t>(ctr), static_cast<uint32_t>(ctr >> 32), 0u,
+                                                   0u, p.k0, p.k1, p.rounds);
+                const uint32_t ln = static_cast<uint32_t>(idx & 3);
+                const uint32_t wd = ln == 0 ? o.x : ln == 1 ? o.y : ln == 2 ? o.z : o.w;
+                w |= static_cast<uint32_t>(wd < p.thr) << c;
+            }
+        }
+    } else {
+        w = 0xFFFFFFFFu;
+    }
+    return n_valid >= 32 ? w : (w & ((1u << n_valid) - 1u));
+}
+
+__global__ void bwd_prep_kernel(const __nv_bfloat16* __restrict__ O, long long o_sb, long long o_sh, long long o_ss,
+                                const __nv_bfloat16* __restrict__ dO, long long d_sb, long long d_sh, long long d_ss,
+                                const float* __restrict__ lse, float* __restrict__ rows, float* __restrict__ dq_acc,
+                                int B, int H, int S, int n_qt, int HD) {
+    const uint64_t padded = static_cast<uint64_t>(n_qt) * BQ;
+    const uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= static_cast<uint64_t>(B) * H * padded) return;
+    const uint64_t slice = t / padded;
+    const int r = static_cast<int>(t - slice * padded);
+    const int qt = r / BQ, rr = r % BQ;
+    const int bb = static_cast<int>(slice / H), hh = static_cast<int>(slice % H);
+    float d = 0.0f, nl = -INFINITY;
+    if (r < S) {
+        const uint4* po = reinterpret_cast<const uint4*>(O + bb * o_sb + hh * o_sh + static_cast<long long>(r) * o_ss);
+        const uint4* pd = reinterpret_cast<const uint4*>(dO + bb * d_sb + hh * d_sh + static_cast<long long>(r) * d_ss);
+        float acc0 = 0.0f, acc1 = 0.0f;
+        for (int c = 0; c < HD / 8; ++c) {
+            const uint4 a = __ldg(po + c), b = __ldg(pd + c);
+            const uint32_t av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                acc0 = fmaf(bf16_lo(av[e]), bf16_lo(bv[e]), acc0);
+                acc1 = fmaf(bf16_hi(av[e]), bf16_hi(bv[e]), acc1);
+            }
+        }
+        d = acc0 + acc1;
+        nl = -lse[slice * S + r] * 1.4426950408889634f;
+    }
+    float* rw = rows + (slice * n_qt + qt) * (2 * BQ);
+    rw[rr] = nl;
+    rw[BQ + rr] = d;
+    float4* acc = reinterpret_cast<float4*>(dq_acc + dq_tile_base(slice, n_qt, qt, HD));
+    for (int g = 0; g < HD / 4; ++g) acc[g * BQ + rr] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+}
+
+__global__ void bwd_dq_kernel(const float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dQ, long long q_sb,
+                              long long q_sh, long long q_ss, int B, int H, int S, int n_qt, int HD, float scale) {
+    // thread = (slice, row, 8-column group): reads 2 float4 (coalesced over
+    // rows), writes 16 bytes of bf16
+    const int groups = HD / 8;
+    const uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t padded = static_cast<uint64_t>(n_qt) * BQ;
+    const uint64_t per_slice = padded * groups;
+    if (t >= static_cast<uint64_t>(B) * H * per_slice) return;
+    const uint64_t slice = t / per_slice;
+    const uint64_t rem = t - slice * per_slice;
+    const int g = static_cast<int>(rem / padded);
+    const int r = static_cast<int>(rem - static_cast<uint64_t>(g) * padded);
+    if (r >= S) return;
+    const int qt = r / BQ, rr = r % BQ;
+    const float4* acc = reinterpret_cast<const float4*>(dq_acc + dq_tile_base(slice, n_qt, qt, HD));
+    const float4 a = acc[(2 * g) * BQ + rr], b = acc[(2 * g + 1) * BQ + rr];
+    const int bb = static_cast<int>(slice / H), hh = static_cast<int>(slice % H);
+    uint4 out;
+    out.x = pack_bf16(a.x * scale, a.y * scale);
+    out.y = pack_bf16(a.z * scale, a.w * scale);
+    out.z = pack_bf16(b.x * scale, b.y * scale);
+    out.w = pack_bf16(b.z * scale, b.w * scale);
+    *reinterpret_cast<uint4*>(dQ + bb * q_sb + hh * q_sh + static_cast<long long>(r) * q_ss + 8 * g) = out;
+}
+
+template <int HD, int MODE, int R>
+__global__ void __launch_bounds__(THREADS, 1) bwd_main_kernel(const __grid_constant__ CUtensorMap tmQ,
+                                                              const __grid_constant__ CUtensorMap tmK,
+                                                              const __grid_constant__ CUtensorMap tmV,
+                                                              const __grid_constant__ CUtensorMap tmdO,
+                                                              const Params p) {
+    using SM = Smem<HD>;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
+    if (pad + SM::BYTES > static_cast<uint32_t>(SM::ALLOC)) __trap();
+    uint8_t* smem = smem_raw + pad;
+    uint8_t* sK = smem + SM::K_OFF;
+    uint8_t* sV = smem + SM::V_OFF;
+    uint8_t* sQ = smem + SM::Q_OFF;
+    uint8_t* sdO = smem + SM::DO_OFF;
+    uint8_t* sdS = smem + SM::DS_OFF;
+    const float* sRows = reinterpret_cast<const float*>(smem + SM::ROW_OFF);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::BAR_OFF);
+    uint64_t* kv_full = bars;
+    uint64_t* q_full = bars + 1;          // [2]
+    uint64_t* q_empty = q_full + STAGES;  // [2]
+    uint64_t* do_full = q_empty + STAGES;
+    uint64_t* do_empty = do_full + STAGES;
+    uint64_t* s_full = do_empty + STAGES;
+    uint64_t* p_full = s_full + 1;
+    uint64_t* dp_full = p_full + 1;
+    uint64_t* ds_full = dp_full + 1;
+    uint64_t* dq_full = ds_full + 1;
+    uint64_t* dq_empty = dq_full + 1;
+    uint64_t* acc_full = dq_empty + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+
+    const uint32_t warp = warp_id(), lane = lane_id();
+    const int kt = blockIdx.x % p.n_kt;
+    const int bh = blockIdx.x / p.n_kt;
+    const int hh = bh % p.H, bb = bh / p.H;
+    const uint64_t slice = static_cast<uint64_t>(bb) * p.H + hh;
+    const int kv0 = kt * BKV;
+    const int n_qt = p.n_qt;
+    constexpr int NCH = HD / 64;
+
+    if (warp == 0 && lane == 0) {
+        mbar_init(smem_u32(kv_full), 1);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(smem_u32(&q_full[s]), 1);
+            mbar_init(smem_u32(&q_empty[s]), 1);
+            mbar_init(smem_u32(&do_full[s]), 1);
+            mbar_init(smem_u32(&do_empty[s]), 1);
+        }
+        mbar_init(smem_u32(s_full), 1);
+        mbar_init(smem_u32(p_full), 8);
+        mbar_init(smem_u32(dp_full), 1);
+        mbar_init(smem_u32(ds_full), 8);
+        mbar_init(smem_u32(dq_full), 1);
+        mbar_init(smem_u32(dq_empty), 4);
+        mbar_init(smem_u32(acc_full), 1);
+        fence_mbar_init();
+        tma_prefetch_desc(&tmQ);
+        tma_prefetch_desc(&tmK);
+        tma_prefetch_desc(&tmV);
+        tma_prefetch_desc(&tmdO);
+    }
+    if (warp == 1) tmem_alloc<TMEM_COLS>(smem_u32(tmem_slot));
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {  // ------------------------------------------------------------ TMA
+        if (elect_one()) {
+            const uint32_t kb = smem_u32(kv_full);
+            mbar_arrive_expect_tx(kb, 2 * SM::TILE);
+            for (int c = 0; c < NCH; ++c) {
+                tma_load_4d(smem_u32(sK + c * SM::CHUNK), &tmK, kb, c * 64, kv0, hh, bb);
+                tma_load_4d(smem_u32(sV + c * SM::CHUNK), &tmV, kb, c * 64, kv0, hh, bb);
+            }
+        }
+        __syncwarp();
+        const float* rows = p.rows + slice * n_qt * (2 * BQ);
+        for (int i = 0; i < n_qt; ++i) {
+            const int st = i & 1;
+            const uint32_t ph = (i >> 1) & 1;
+            mbar_wait(smem_u32(&q_empty[st]), ph ^ 1);
+            if (elect_one()) {
+                const uint32_t qb = smem_u32(&q_full[st]);
+                mbar_arrive_expect_tx(qb, SM::TILE + 1024);
+                for (int c = 0; c < NCH; ++c)
+                    tma_load_4d(smem_u32(sQ + st * SM::TILE + c * SM::CHUNK), &tmQ, qb, c * 64, i * BQ, hh, bb);
+                bulk_load(smem_u32(smem + SM::ROW_OFF + st * 1024), rows + i * (2 * BQ), 1024, qb);
+            }
+            __syncwarp();
+            mbar_wait(smem_u32(&do_empty[st]), ph ^ 1);
+            if (elect_one()) {
+                const uint32_t db = smem_u32(&do_full[st]);
+                mbar_arrive_expect_tx(db, SM::TILE);
+                for (int c = 0; c < NCH; ++c)
+                    tma_load_4d(smem_u32(sdO + st * SM::TILE + c * SM::CHUNK), &tmdO, db, c * 64, i * BQ, hh, bb);
+            }
+            __syncwarp();
+        }
+    } else if (warp == 1) {  // ----------------------------------------------------- MMA
+        constexpr uint32_t IDESC_T = idesc_make(1, 1, BKV, BQ, 0, 0);   // S^T, dP^T
+        constexpr uint32_t IDESC_ACC = idesc_make(1, 1, BKV, HD, 0, 1); // dV, dK (A TMEM, B MN-major)
+        constexpr uint32_t IDESC_DQ = idesc_make(1, 1, BQ, HD, 1, 1);   // dQ (A, B MN-major)
+        const uint64_t k_kdesc = desc_kmajor_sw128(smem_u32(sK));
+        const uint64_t v_kdesc = desc_kmajor_sw128(smem_u32(sV));
+        const uint64_t q_kdesc = desc_kmajor_sw128(smem_u32(sQ));
+        const uint64_t do_kdesc = desc_kmajor_sw128(smem_u32(sdO));
+        const uint64_t q_mdesc = desc_sw128(smem_u32(sQ), SM::CHUNK, 1024);
+        const uint64_t do_mdesc = desc_sw128(smem_u32(sdO), SM::CHUNK, 1024);
+        const uint64_t k_mdesc = desc_sw128(smem_u32(sK), SM::CHUNK, 1024);
+        const uint64_t ds_mdesc = desc_sw128(smem_u32(sdS), SM::CHUNK, 1024);
+        const uint32_t tS = tmem, tdP = tmem + 128, tdV = tmem + 256, tdK = tmem + 256 + HD;
+        // D (128 x 128) = A (128 x HD, K-major) . B (128 x HD, K-major)^T
+        auto issue_t = [&](uint32_t d, uint64_t a, uint64_t b) {
+#pragma unroll
+            for (int kk = 0; kk < HD / 16; ++kk) {
+                const uint32_t off = ((kk >> 2) * SM::CHUNK + (kk & 3) * 32) >> 4;
+                mma_f16_ss(d, a + off, b + off, IDESC_T, kk > 0);
+            }
+        };
+        // D (128 keys x HD) += A^T from TMEM (bf16 pairs: queries 64h+16m.. at
+        // column 64h + 8m) . B (128 queries x HD, MN-major)
+        auto issue_acc = [&](uint32_t d, uint32_t a_tmem, uint64_t b, bool acc) {
+#pragma unroll
+            for (int kk = 0; kk < BQ / 16; ++kk)
+                mma_f16_ts(d, a_tmem + (kk >> 2) * 64 + (kk & 3) * 8, b + ((kk * 2048) >> 4), IDESC_ACC,
+                           (acc || kk > 0) ? 1u : 0u);
+        };
+        mbar_wait(smem_u32(kv_full), 0);
+        mbar_wait(smem_u32(&q_full[0]), 0);
+        tc_fence_after();
+        if (elect_one()) {
+            issue_t(tS, k_kdesc, q_kdesc);
+            tc_commit(smem_u32(s_full));
+        }
+        __syncwarp();
+        for (int i = 0; i < n_qt; ++i) {
+            const int st = i & 1;
+            const uint32_t ph = (i >> 1) & 1;
+            const uint32_t soff = (st * SM::TILE) >> 4;
+            mbar_wait(smem_u32(&do_full[st]), ph);
+            if (i > 0) mbar_wait(smem_u32(dq_empty), (i - 1) & 1);
+            tc_fence_after();
+            if (elect_one()) {
+                issue_t(tdP, v_kdesc, do_kdesc + soff);
+                tc_commit(smem_u32(dp_full));
+            }
+            __syncwarp();
+            mbar_wait(smem_u32(p_full), i & 1);
+            tc_fence_after();
+            if (elect_one()) {
+                issue_acc(tdV, tS, do_mdesc + soff, i > 0);
+                tc_commit(smem_u32(&do_empty[st]));
+            }
+            __syncwarp();
+            if (i + 1 < n_qt) {
+                const int st1 = (i + 1) & 1;
+                mbar_wait(smem_u32(&q_full[st1]), ((i + 1) >> 1) & 1);
+                tc_fence_after();
+                if (elect_one()) {
+                    issue_t(tS, k_kdesc, q_kdesc + ((st1 * SM::TILE) >> 4));
+                    tc_commit(smem_u32(s_full));
+                }
+                __syncwarp();
+            }
+            mbar_wait(smem_u32(ds_full), i & 1);
+            tc_fence_after();
+            if (elect_one()) {
+                issue_acc(tdK, tdP, q_mdesc + soff, i > 0);
+#pragma unroll
+                for (int kk = 0; kk < BKV / 16; ++kk)
+                    mma_f16_ss(tdP, ds_mdesc + ((kk * 2048) >> 4), k_mdesc + ((kk * 2048) >> 4), IDESC_DQ, kk > 0);
+                tc_commit(smem_u32(&q_empty[st]));
+                tc_commit(smem_u32(dq_full));
+                if (i + 1 == n_qt) tc_commit(smem_u32(acc_full));
+            }
+            __syncwarp();
+        }
+    } else if (warp >= 4 && warp < 12) {  // --------------------------------- softmax / dS
+        const int h = (warp - 4) >> 2;         // query half of each tile
+        const uint32_t qw = warp & 3;          // TMEM lane quarter
+        const int r = static_cast<int>(qw * 32 + lane);  // key row within the CTA tile
+        const bool key_valid = kv0 + r < p.S;
+        const uint32_t lane_base = (qw * 32) << 16;
+        const uint32_t tS = tmem + lane_base + 64 * h;
+        const uint32_t tdP = tmem + lane_base + 128 + 64 * h;
+        const int kcol = kv0 + static_cast<int>(qw) * 32;  // first key of this warp's 32
+        const int kvalid = p.S - kcol;                     // valid keys in the warp's word
+        uint8_t* ds_row = sdS + h * SM::CHUNK + r * 128;
+        const uint32_t sw = static_cast<uint32_t>(r & 7);
+        const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
+        for (int i = 0; i < n_qt; ++i) {
+            const int st = i & 1;
+            const uint32_t ph = (i >> 1) & 1;
+            // keep words: bit e of kt[c] = keep(query i*128 + 64h + 32c + e, key kv0 + r)
+            uint32_t kt[2];
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const int qrow = i * BQ + 64 * h + 32 * c + static_cast<int>(lane);
+                uint32_t w = 0;
+                if (qrow < p.S) w = row_word<MODE, R>(p, (slice * p.S + qrow) * static_cast<uint64_t>(p.S) + kcol, kvalid);
+                kt[c] = transpose32(w, lane);
+            }
+            if (!key_valid) kt[0] = kt[1] = 0;
+            const float* nlse = sRows + st * 256 + 64 * h;
+            const float* Dv = nlse + BQ;
+            mbar_wait(smem_u32(&q_full[st]), ph);  // rows of tile i landed (already complete)
+            mbar_wait(smem_u32(s_full), i & 1);
+            tc_fence_after();
+            // ---- P phase: P = 2^(s*scale*log2e - lse*log2e); W = keep ? P : 0 -> TMEM (bf16)
+            uint32_t pb[2][16];
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                uint32_t s[32];
+                tmem_ld32(tS + 32 * c, s);
+                tmem_ld_wait_regs(s);
+                uint32_t wpk[16];
+#pragma unroll
+                for (int e = 0; e < 32; e += 4) {
+                    const float4 nl = *reinterpret_cast<const float4*>(nlse + 32 * c + e);
+                    const float2 t0 = __ffma2_rn(make_float2(__uint_as_float(s[e]), __uint_as_float(s[e + 1])), sc2,
+                                                 make_float2(nl.x, nl.y));
+                    const float2 t1 = __ffma2_rn(make_float2(__uint_as_float(s[e + 2]), __uint_as_float(s[e + 3])),
+                                                 sc2, make_float2(nl.z, nl.w));
+                    const float p0 = ex2_approx(t0.x), p1 = ex2_approx(t0.y);
+                    const float p2 = ex2_approx(t1.x), p3 = ex2_approx(t1.y);
+                    pb[c][e / 2] = pack_bf16(p0, p1);
+                    pb[c][e / 2 + 1] = pack_bf16(p2, p3);
+                    wpk[e / 2] = pack_bf16(((kt[c] >> e) & 1u) ? p0 : 0.0f, ((kt[c] >> (e + 1)) & 1u) ? p1 : 0.0f);
+                    wpk[e / 2 + 1] =
+                        pack_bf16(((kt[c] >> (e + 2)) & 1u) ? p2 : 0.0f, ((kt[c] >> (e + 3)) & 1u) ? p3 : 0.0f);
+                }
+                tmem_st16(tS + 16 * c, wpk);
+            }
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(p_full));
+            // ---- dS phase: dS = P o (keep ? dP/p : 0 - D) -> TMEM (bf16, for dK) and smem (for dQ)
+            mbar_wait(smem_u32(dp_full), i & 1);
+            tc_fence_after();
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                uint32_t d[32];
+                tmem_ld32(tdP + 32 * c, d);
+                tmem_ld_wait_regs(d);
+                uint32_t dpk[16];
+#pragma unroll
+                for (int e = 0; e < 32; e += 4) {
+                    const float4 dd = *reinterpret_cast<const float4*>(Dv + 32 * c + e);
+                    const float dv[4] = {dd.x, dd.y, dd.z, dd.w};
+                    float ds[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const uint32_t pw = pb[c][(e + u) / 2];
+                        const float pv = ((e + u) & 1) ? bf16_hi(pw) : bf16_lo(pw);
+                        const float dp = ((kt[c] >> (e + u)) & 1u) ? __uint_as_float(d[e + u]) * p.inv_keep : 0.0f;
+                        ds[u] = pv * (dp - dv[u]);
+                    }
+                    dpk[e / 2] = pack_bf16(ds[0], ds[1]);
+                    dpk[e / 2 + 1] = pack_bf16(ds[2], ds[3]);
+                }
+                tmem_st16(tdP + 16 * c, dpk);
+                // smem dS row (key r), queries 64h + 32c.. : 16-byte units 4c..4c+3 of line r
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t unit = (4 * c + u) ^ sw;
+                    *reinterpret_cast<uint4*>(ds_row + unit * 16) =
+                        make_uint4(dpk[4 * u], dpk[4 * u + 1], dpk[4 * u + 2], dpk[4 * u + 3]);
+                }
+            }
+            fence_proxy_async_smem();
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(ds_full));
+        }
+        // ---- epilogue: dV = acc / keep_prob, dK = acc * scale; columns [h*HD/2, (h+1)*HD/2)
+        mbar_wait(smem_u32(acc_full), 0);
+        tc_fence_after();
+        const int key = kv0 + r;
+        __nv_bfloat16* dv_row = static_cast<__nv_bfloat16*>(p.dV) + bb * p.v_sb + hh * p.v_sh +
+                                static_cast<long long>(key_valid ? key : 0) * p.v_ss;
+        __nv_bfloat16* dk_row = static_cast<__nv_bfloat16*>(p.dK) + bb * p.k_sb + hh * p.k_sh +
+                                static_cast<long long>(key_valid ? key : 0) * p.k_ss;
+#pragma unroll 1
+        for (int which = 0; which < 2; ++which) {
+            const uint32_t tacc = tmem + lane_base + 256 + which * HD;
+            const float mul = which == 0 ? p.inv_keep : p.scale;
+            __nv_bfloat16* dst = which == 0 ? dv_row : dk_row;
+#pragma unroll 1
+            for (int c = 0; c < HD / 64; ++c) {
+                const int col = h * (HD / 2) + 32 * c;
+                uint32_t o[32];
+                tmem_ld32(tacc + col, o);
+                tmem_ld_wait_regs(o);
+                uint32_t pk[16];
+#pragma unroll
+                for (int e = 0; e < 16; ++e)
+                    pk[e] = pack_bf16(__uint_as_float(o[2 * e]) * mul, __uint_as_float(o[2 * e + 1]) * mul);
+                if (key_valid) {
+                    uint4* d4 = reinterpret_cast<uint4*>(dst + col);
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) d4[v] = make_uint4(pk[4 * v], pk[4 * v + 1], pk[4 * v + 2], pk[4 * v + 3]);
+                }
+            }
+        }
+    } else if (warp >= 12) {  // ------------------------------------------------- dQ drain
+        const uint32_t qw = warp & 3;
+        const int r = static_cast<int>(qw * 32 + lane);
+        const uint32_t tdq = tmem + ((qw * 32) << 16) + 128;
+        for (int i = 0; i < n_qt; ++i) {
+            mbar_wait(smem_u32(dq_full), i & 1);
+            tc_fence_after();
+            float* acc = p.dq_acc + dq_tile_base(slice, n_qt, i, HD);
+#pragma unroll 1
+            for (int c = 0; c < HD / 32; ++c) {
+                uint32_t v[32];
+                tmem_ld32(tdq + 32 * c, v);
+                tmem_ld_wait_regs(v);
+                if (c == HD / 32 - 1) {  // all of this warp's TMEM reads are done
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(smem_u32(dq_empty));
+                }
+#pragma unroll
+                for (int g = 0; g < 8; ++g)
+                    red_add_v4(acc + dq_off(r, 32 * c + 4 * g), __uint_as_float(v[4 * g]), __uint_as_float(v[4 * g + 1]),
+                               __uint_as_float(v[4 * g + 2]), __uint_as_float(v[4 * g + 3]));
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc<TMEM_COLS>(tmem);
+}
+
+template <int HD, int MODE, int R>
+static cudaError_t launch_main(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
+                               const CUtensorMap& dO, const Params& p, cudaStream_t s) {
+    auto kern = bwd_main_kernel<HD, MODE, R>;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<HD>::ALLOC);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    const unsigned grid = static_cast<unsigned>(p.B) * p.H * p.n_kt;
+    kern<<<grid, THREADS, Smem<HD>::ALLOC, s>>>(q, k, v, dO, p);
+    return cudaGetLastError();
+}
+
+}  // namespace rgo_attn_bwd
+
+namespace rgo {
+
+uint64_t attn_bwd_workspace_bytes(int B, int H, int S, int HD) {
+    const uint64_t n_qt = (S + rgo_attn_bwd::BQ - 1) / rgo_attn_bwd::BQ;
+    const uint64_t rows = static_cast<uint64_t>(B) * H * n_qt * rgo_attn_bwd::BQ;
+    return rows * HD * 4 + rows * 2 * 4;
+}
+
+static bool tmap4(CUtensorMap* m, const AttnTensor& t, int B, int H, int S, int HD) {
+    const uint64_t dims[4] = {static_cast<uint64_t>(HD), static_cast<uint64_t>(S), static_cast<uint64_t>(H),
+                              static_cast<uint64_t>(B)};
+    const uint64_t strides[3] = {static_cast<uint64_t>(t.ss) * 2, static_cast<uint64_t>(t.sh) * 2,
+                                 static_cast<uint64_t>(t.sb) * 2};
+    const uint32_t box[4] = {64, 128, 1, 1};
+    return make_tmap(m, t.ptr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+cudaError_t launch_attn_bwd(const AttnBwdJob& j, cudaStream_t s) {
+    using namespace rgo_attn_bwd;
+    CUtensorMap tq, tk, tv, tdo;
+    if (!tmap4(&tq, j.q, j.B, j.H, j.S, j.HD) || !tmap4(&tk, j.k, j.B, j.H, j.S, j.HD) ||
+        !tmap4(&tv, j.v, j.B, j.H, j.S, j.HD) || !tmap4(&tdo, j.dout, j.B, j.H, j.S, j.HD))
+        return cudaErrorInvalidResourceHandle;  // tensor-map encode rejected a view
+    const int n_qt = (j.S + BQ - 1) / BQ;
+    const uint64_t rows = static_cast<uint64_t>(j.B) * j.H * n_qt * BQ;
+    float* dq_acc = static_cast<float*>(j.work);
+    float* rowbuf = dq_acc + rows * j.HD;
+    {
+        const unsigned threads = 256;
+        const unsigned grid = static_cast<unsigned>((rows + threads - 1) / threads);
+        bwd_prep_kernel<<<grid, threads, 0, s>>>(static_cast<const __nv_bfloat16*>(j.o.ptr), j.o.sb, j.o.sh, j.o.ss,
+                                                 static_cast<const __nv_bfloat16*>(j.dout.ptr), j.dout.sb, j.dout.sh,
+                                                 j.dout.ss, j.lse, rowbuf, dq_acc, j.B, j.H, j.S, n_qt, j.HD);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    Params p{};
+    p.B = j.B; p.H = j.H; p.S = j.S;
+    p.n_qt = n_qt;
+    p.n_kt = (j.S + BKV - 1) / BKV;
+    p.scale = j.scale;
+    p.scale_log2 = j.scale * 1.4426950408889634f;
+    p.inv_keep = 1.0f / (j.mode == rgo_attn::MASK_NONE ? 1.0f : j.keep_prob);
+    p.bits = j.bits;
+    p.bits_bytes = j.bits_bytes;
+    p.bits_aligned = (j.S % 32) == 0 && (reinterpret_cast<uintptr_t>(j.bits) & 3) == 0;
+    p.k0 = static_cast<uint32_t>(j.seed);
+    p.k1 = static_cast<uint32_t>(j.seed >> 32);
+    p.base_offset = j.base_offset;
+    p.thr = static_cast<uint32_t>(j.threshold);
+    p.rounds = j.rounds;
+    p.rows = rowbuf;
+    p.dq_acc = dq_acc;
+    p.dK = j.dk.ptr; p.k_sb = j.dk.sb; p.k_sh = j.dk.sh; p.k_ss = j.dk.ss;
+    p.dV = j.dv.ptr; p.v_sb = j.dv.sb; p.v_sh = j.dv.sh; p.v_ss = j.dv.ss;
+    int mode = j.mode;
+    if (mode == rgo_attn::MASK_PHILOX && j.threshold >= (uint64_t{1} << 32)) mode = rgo_attn::MASK_NONE;
+    cudaError_t e = cudaErrorInvalidValue;
+#define RGO_B(HDV, MODEV, RV) \
+    if (j.HD == HDV && mode == MODEV) { e = launch_main<HDV, MODEV, RV>(tq, tk, tv, tdo, p, s); goto launched; }
+    RGO_B(128, MASK_NONE, 0)
+    RGO_B(64, MASK_NONE, 0)
+    RGO_B(128, MASK_BITS, 0)
+    RGO_B(64, MASK_BITS, 0)
+    if (mode == rgo_attn::MASK_PHILOX) {
+        if (j.rounds == 10) {
+            RGO_B(128, MASK_PHILOX, 10)
+            RGO_B(64, MASK_PHILOX, 10)
+        } else if (j.rounds == 7) {
+            RGO_B(128, MASK_PHILOX, 7)
+            RGO_B(64, MASK_PHILOX, 7)
+        } else {
+            RGO_B(128, MASK_PHILOX, 0)
+            RGO_B(64, MASK_PHILOX, 0)
+        }
+    }
+#undef RGO_B
+    return cudaErrorNotSupported;
+launched:
+    if (e != cudaSuccess) return e;
+    {
+        const unsigned threads = 256;
+        const uint64_t n = rows * (j.HD / 8);
+        const unsigned grid = static_cast<unsigned>((n + threads - 1) / threads);
+        bwd_dq_kernel<<<grid, threads, 0, s>>>(dq_acc, static_cast<__nv_bfloat16*>(j.dq.ptr), j.dq.sb, j.dq.sh,
+                                               j.dq.ss, j.B, j.H, j.S, n_qt, j.HD, j.scale);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace rgo

@@ -42,6 +42,11 @@ int require_device() {
         cudaGetLastError();
         return fail(RGO_ENODEV, "no CUDA device: the rgo B200 path has no CPU fallback");
     }
+    // Drop a non-sticky error that other code left in this host thread's
+    // runtime state (e.g. torch's autograd worker threads), so the launch
+    // checks that follow report only this call's launches.  A sticky error
+    // still fails the launch itself.
+    cudaGetLastError();
     return RGO_OK;
 }
 
@@ -314,16 +319,15 @@ int rgo_gemm_with_rng(const rgo_gemm_desc* g, const void* d_a, const void* d_b, 
     return ce == cudaSuccess ? RGO_OK : cuda_fail(ce, "rgo_gemm_with_rng");
 }
 
-int rgo_attn_fwd(const rgo_attn_desc* a, const rgo_tensor4* q, const rgo_tensor4* k,
-                 const rgo_tensor4* v, const uint8_t* d_bits, uint64_t bits_bytes,
-                 const rgo_tensor4* o, float* d_lse, rgo_stream_t stream) {
-    if (!a || !q || !k || !v || !o) return fail(RGO_EINVAL, "rgo_attn_fwd: null argument");
+// Validation shared by the forward and backward (ref_attention.hpp:117-118,
+// :131-139 for the dropout arguments).
+static int attn_check(const char* fn, const rgo_attn_desc* a, const uint8_t* d_bits, uint64_t bits_bytes) {
     if (a->batch < 1 || a->heads < 1 || a->seq < 1 || a->head_dim < 1)
         return fail(RGO_EINVAL, "attention dims must be >= 1");
     if (a->head_dim != 64 && a->head_dim != 128)
-        return fail(RGO_EINVAL, "rgo_attn_fwd: head_dim must be 64 or 128 (pad smaller heads)");
+        return fail(RGO_EINVAL, "%s: head_dim must be 64 or 128 (pad smaller heads)", fn);
     if (a->mask_source < RGO_MASK_NONE || a->mask_source > RGO_MASK_PHILOX)
-        return fail(RGO_EINVAL, "rgo_attn_fwd: bad mask source");
+        return fail(RGO_EINVAL, "%s: bad mask source", fn);
     const bool drop = a->mask_source != RGO_MASK_NONE;
     if (drop && !(a->keep_prob > 0.0 && a->keep_prob <= 1.0))  // ref_attention.hpp:117-118
         return fail(RGO_EINVAL, "attention_dropout: p must be in (0,1]");
@@ -333,27 +337,32 @@ int rgo_attn_fwd(const rgo_attn_desc* a, const rgo_tensor4* q, const rgo_tensor4
                     static_cast<unsigned long long>((n + 7) / 8));
     if (a->mask_source == RGO_MASK_PHILOX && (a->rounds < 1 || a->rounds > 16))
         return fail(RGO_EINVAL, "attention_dropout_fused: rounds must be in [1,16]");
-    const rgo_tensor4* ts[4] = {q, k, v, o};
-    for (const rgo_tensor4* t : ts) {
-        if (!t->ptr || (reinterpret_cast<uintptr_t>(t->ptr) & 15) || ((t->stride_b | t->stride_h | t->stride_s) * 2) % 16)
-            return fail(RGO_EINVAL, "rgo_attn_fwd: tensors need 16-byte aligned base and strides");
+    return RGO_OK;
+}
+
+static int tensors_ok(const char* fn, const rgo_tensor4* const* ts, int n) {
+    for (int i = 0; i < n; ++i) {
+        const rgo_tensor4* t = ts[i];
+        if (!t || !t->ptr || (reinterpret_cast<uintptr_t>(t->ptr) & 15) ||
+            ((t->stride_b | t->stride_h | t->stride_s) * 2) % 16)
+            return fail(RGO_EINVAL, "%s: tensors need 16-byte aligned base and strides", fn);
     }
-    if (int e = require_device()) return e;
-    rgo::AttnJob j{};
+    return RGO_OK;
+}
+
+extern "C++" {
+// The dropout fields shared by AttnJob and AttnBwdJob.
+template <class J>
+static void attn_fill(J& j, const rgo_attn_desc* a, const uint8_t* d_bits, uint64_t bits_bytes) {
     j.B = static_cast<int>(a->batch);
     j.H = static_cast<int>(a->heads);
     j.S = static_cast<int>(a->seq);
     j.HD = static_cast<int>(a->head_dim);
     j.scale = a->scale > 0 ? a->scale : 1.0f / std::sqrt(static_cast<float>(a->head_dim));
-    j.q = {q->ptr, q->stride_b, q->stride_h, q->stride_s};
-    j.k = {k->ptr, k->stride_b, k->stride_h, k->stride_s};
-    j.v = {v->ptr, v->stride_b, v->stride_h, v->stride_s};
-    j.o = {const_cast<void*>(o->ptr), o->stride_b, o->stride_h, o->stride_s};
-    j.lse = d_lse;
     j.mode = a->mask_source;
     float kp = 1.0f;
     uint64_t thr = uint64_t{1} << 32;
-    rgo_keep_threshold(drop ? a->keep_prob : 1.0, &thr, &kp);
+    rgo_keep_threshold(a->mask_source != RGO_MASK_NONE ? a->keep_prob : 1.0, &thr, &kp);
     j.keep_prob = kp;
     j.threshold = thr;
     j.bits = d_bits;
@@ -361,8 +370,71 @@ int rgo_attn_fwd(const rgo_attn_desc* a, const rgo_tensor4* q, const rgo_tensor4
     j.seed = a->seed;
     j.base_offset = a->base_offset;
     j.rounds = static_cast<int>(a->rounds);
+}
+
+static rgo::AttnTensor view(const rgo_tensor4* t) { return {t->ptr, t->stride_b, t->stride_h, t->stride_s}; }
+static rgo::AttnOut view_out(const rgo_tensor4* t) {
+    return {const_cast<void*>(t->ptr), t->stride_b, t->stride_h, t->stride_s};
+}
+}  // extern "C++"
+
+int rgo_attn_fwd(const rgo_attn_desc* a, const rgo_tensor4* q, const rgo_tensor4* k,
+                 const rgo_tensor4* v, const uint8_t* d_bits, uint64_t bits_bytes,
+                 const rgo_tensor4* o, float* d_lse, rgo_stream_t stream) {
+    if (!a || !q || !k || !v || !o) return fail(RGO_EINVAL, "rgo_attn_fwd: null argument");
+    if (int e = attn_check("rgo_attn_fwd", a, d_bits, bits_bytes)) return e;
+    const rgo_tensor4* ts[4] = {q, k, v, o};
+    if (int e = tensors_ok("rgo_attn_fwd", ts, 4)) return e;
+    if (int e = require_device()) return e;
+    rgo::AttnJob j{};
+    attn_fill(j, a, d_bits, bits_bytes);
+    j.q = view(q);
+    j.k = view(k);
+    j.v = view(v);
+    j.o = view_out(o);
+    j.lse = d_lse;
     cudaError_t ce = rgo::launch_attn_fwd(j, static_cast<cudaStream_t>(stream));
     return ce == cudaSuccess ? RGO_OK : cuda_fail(ce, "rgo_attn_fwd");
+}
+
+int rgo_attn_bwd_workspace(const rgo_attn_desc* a, uint64_t* bytes) {
+    if (!a || !bytes) return fail(RGO_EINVAL, "rgo_attn_bwd_workspace: null argument");
+    if (a->batch < 1 || a->heads < 1 || a->seq < 1 || (a->head_dim != 64 && a->head_dim != 128))
+        return fail(RGO_EINVAL, "rgo_attn_bwd_workspace: bad dims (head_dim must be 64 or 128)");
+    *bytes = rgo::attn_bwd_workspace_bytes(static_cast<int>(a->batch), static_cast<int>(a->heads),
+                                           static_cast<int>(a->seq), static_cast<int>(a->head_dim));
+    return RGO_OK;
+}
+
+int rgo_attn_bwd(const rgo_attn_desc* a, const rgo_tensor4* q, const rgo_tensor4* k, const rgo_tensor4* v,
+                 const rgo_tensor4* o, const rgo_tensor4* d_o, const float* d_lse, const uint8_t* d_bits,
+                 uint64_t bits_bytes, const rgo_tensor4* dq, const rgo_tensor4* dk, const rgo_tensor4* dv,
+                 void* d_work, uint64_t work_bytes, rgo_stream_t stream) {
+    if (!a || !q || !k || !v || !o || !d_o || !dq || !dk || !dv || !d_lse)
+        return fail(RGO_EINVAL, "rgo_attn_bwd: null argument");
+    if (int e = attn_check("rgo_attn_bwd", a, d_bits, bits_bytes)) return e;
+    const rgo_tensor4* ts[8] = {q, k, v, o, d_o, dq, dk, dv};
+    if (int e = tensors_ok("rgo_attn_bwd", ts, 8)) return e;
+    const uint64_t need = rgo::attn_bwd_workspace_bytes(static_cast<int>(a->batch), static_cast<int>(a->heads),
+                                                        static_cast<int>(a->seq), static_cast<int>(a->head_dim));
+    if (!d_work || work_bytes < need || (reinterpret_cast<uintptr_t>(d_work) & 15))
+        return fail(RGO_EINVAL, "rgo_attn_bwd: workspace needs %llu bytes (16-byte aligned)",
+                    static_cast<unsigned long long>(need));
+    if (int e = require_device()) return e;
+    rgo::AttnBwdJob j{};
+    attn_fill(j, a, d_bits, bits_bytes);
+    j.q = view(q);
+    j.k = view(k);
+    j.v = view(v);
+    j.o = view(o);
+    j.dout = view(d_o);
+    j.dq = view_out(dq);
+    j.dk = view_out(dk);
+    j.dv = view_out(dv);
+    j.lse = d_lse;
+    j.work = d_work;
+    cudaError_t ce = rgo::launch_attn_bwd(j, static_cast<cudaStream_t>(stream));
+    return ce == cudaSuccess ? RGO_OK : cuda_fail(ce, "rgo_attn_bwd");
 }
 
 struct rgo_block {

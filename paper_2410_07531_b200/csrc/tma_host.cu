@@ -28,6 +28,11 @@ bool make_tmap(CUtensorMap* map, const void* base, CUtensorMapDataType dtype, ui
                CUtensorMapSwizzle swizzle) {
     auto fn = encode_fn();
     if (!fn) return false;
+    // The driver encoder needs a current context; a host thread that has not
+    // touched the runtime yet (torch's autograd workers, user threads) has
+    // none until the runtime binds the device's primary context.
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaSetDevice(dev) != cudaSuccess) return false;
     cuuint32_t elem_strides[5] = {1, 1, 1, 1, 1};
     cuuint64_t d[5], s[4];
     cuuint32_t b[5];

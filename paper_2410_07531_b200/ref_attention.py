@@ -88,6 +88,71 @@ def attn_fwd(q, k, v, o=None, *, mask_source=MASK_NONE, keep_prob=1.0, bits=None
     return o
 
 
+def attn_bwd(q, k, v, o, do, lse, *, mask_source=MASK_NONE, keep_prob=1.0, bits=None, seed=0, base_offset=0,
+             rounds=10, scale=0.0, dq=None, dk=None, dv=None, work=None, stream=None):
+    """Device-level K7 (csrc/attn_bwd_sm100.cu): dQ, dK, dV (bf16 [B, H, S, D])
+    of the K5/K6 forward with the same mask arguments; o and lse are that
+    forward's output and natural-log LSE, do the incoming gradient."""
+    import torch
+    B, H, S, D = q.shape
+    dev = q.device
+    dq = torch.empty(B, H, S, D, dtype=torch.bfloat16, device=dev) if dq is None else dq
+    dk = torch.empty(B, H, S, D, dtype=torch.bfloat16, device=dev) if dk is None else dk
+    dv = torch.empty(B, H, S, D, dtype=torch.bfloat16, device=dev) if dv is None else dv
+
+    def t4(t):
+        return _lib.tensor4(t.data_ptr(), t.stride(0), t.stride(1), t.stride(2))
+
+    a = _lib.attn_desc(B, H, S, D, scale, mask_source, keep_prob, seed, base_offset, rounds, 0)
+    need = _lib.C.c_uint64()
+    _lib.check(_lib.lib().rgo_attn_bwd_workspace(a, _lib.C.byref(need)))
+    if work is None or work.numel() * work.element_size() < need.value:
+        work = torch.empty((need.value + 15) // 16 * 16, dtype=torch.uint8, device=dev)
+    s = (stream or torch.cuda.current_stream()).cuda_stream
+    _lib.check(_lib.lib().rgo_attn_bwd(a, t4(q), t4(k), t4(v), t4(o), t4(do), lse.data_ptr(),
+                                       bits.data_ptr() if bits is not None else None,
+                                       bits.numel() if bits is not None else 0, t4(dq), t4(dk), t4(dv),
+                                       work.data_ptr(), work.numel() * work.element_size(), s))
+    return dq, dk, dv
+
+
+class DropoutAttention:
+    """torch.autograd.Function over K5/K6 (forward) and K7 (backward):
+    ``DropoutAttention.apply(q, k, v, mask_source, keep_prob, bits, seed,
+    base_offset, rounds)`` with bf16 [B, H, S, D] tensors.  The keep bits of
+    the backward are the forward's (same mask buffer or Philox stream)."""
+
+    _fn = None
+
+    @classmethod
+    def apply(cls, *args):
+        if cls._fn is None:
+            import torch
+
+            class _F(torch.autograd.Function):
+                @staticmethod
+                def forward(ctx, q, k, v, mask_source, keep_prob, bits, seed, base_offset, rounds):
+                    B, H, S, D = q.shape
+                    lse = torch.empty(B * H * S, dtype=torch.float32, device=q.device)
+                    o = attn_fwd(q, k, v, mask_source=mask_source, keep_prob=keep_prob, bits=bits, seed=seed,
+                                 base_offset=base_offset, rounds=rounds, lse=lse)
+                    ctx.save_for_backward(q, k, v, o, lse, bits if bits is not None else torch.empty(0))
+                    ctx.args = (mask_source, keep_prob, seed, base_offset, rounds, bits is not None)
+                    return o
+
+                @staticmethod
+                def backward(ctx, do):
+                    q, k, v, o, lse, bits = ctx.saved_tensors
+                    mask_source, keep_prob, seed, base_offset, rounds, has_bits = ctx.args
+                    dq, dk, dv = attn_bwd(q, k, v, o, do.contiguous(), lse, mask_source=mask_source,
+                                          keep_prob=keep_prob, bits=bits if has_bits else None, seed=seed,
+                                          base_offset=base_offset, rounds=rounds)
+                    return dq, dk, dv, None, None, None, None, None, None
+
+            cls._fn = _F
+        return cls._fn.apply(*args)
+
+
 def _run(inp: AttentionInput, mask_source, keep_prob=1.0, bits=None, seed=0, base_offset=0, rounds=7):
     import torch
     inp.validate()
