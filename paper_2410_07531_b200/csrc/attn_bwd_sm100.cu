@@ -26,16 +26,17 @@
 //                dK  += dS^T Q     (TS: dS^T bf16 from TMEM, Q MN-major)
 //                dQ_i = dS K       (SS: dS MN-major from smem, K MN-major) -> TMEM [128,..)
 //              keys on TMEM lanes (one thread per key row), so dV/dK
-//              accumulate in TMEM for the whole loop; dQ tiles are reduced
-//              into an fp32 accumulator with coalesced red.global.add.v4.f32.
+//              accumulate in TMEM for the whole loop; dQ tiles are staged
+//              through shared memory and reduced into an fp32 accumulator
+//              with TMA bulk reduce-adds (cp.reduce.async.bulk .add.f32).
 //   bwd_dq     dQ = scale * accumulator -> bf16
 //
 // Warp roles of bwd_main (512 threads, 128 registers each):
-//   warp 0      TMA: K, V once; Q (+ its -lse2 / D rows) and dO through 2-stage rings
+//   warp 0      TMA: K, V once; Q (+ its -lse2 / D rows) through a 2-stage ring, dO single-buffered
 //   warp 1      MMA issuer (one elected lane)
 //   warps 4-7   "softmax" WG 0: queries [0,64) of each tile, one thread per key
 //   warps 8-11  softmax WG 1: queries [64,128)
-//   warps 12-15 dQ drain: TMEM -> red.global.add.v4.f32
+//   warps 12-15 dQ drain: TMEM -> smem -> bulk reduce-add into the fp32 accumulator
 // Per query tile i the MMA order is  dP(i), dV(i), S(i+1), dK(i), dQ(i):
 // the softmax's P phase of tile i overlaps dK(i-1)/dQ(i-1)/dP(i), its dS
 // phase overlaps dV(i)/S(i+1).
@@ -47,6 +48,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "attn.h"
 #include "philox.cuh"
@@ -62,7 +64,8 @@ using rgo_attn::MASK_PHILOX;
 
 constexpr int BQ = 128;   // queries per tile
 constexpr int BKV = 128;  // keys per CTA
-constexpr int STAGES = 2;
+constexpr int STAGES = 2;     // Q (+ row terms) ring
+constexpr int DO_STAGES = 1;  // dO is consumed early in each iteration (dP, dV)
 constexpr int THREADS = 512;
 constexpr uint32_t TMEM_COLS = 512;
 constexpr int MAX_DSMEM = 232448;  // 227 KiB opt-in maximum on sm_100
@@ -85,11 +88,12 @@ struct Params {
     void* dV;
     long long k_sb, k_sh, k_ss;  // dK strides (elements)
     long long v_sb, v_sh, v_ss;  // dV strides
+    int debug;                   // experiment switches (RGO_BWD_DEBUG), 0 in production
 };
 
 // Blocked dQ accumulator: per (slice, query tile) HD/32 column chunks of 8
-// groups x 128 rows x float4, so the 32 lanes of a drain warp (32 consecutive
-// rows) add 512 contiguous bytes per instruction.
+// groups x 128 rows x float4 -- the drain's smem staging layout, so each
+// 64-column half of a tile is one contiguous 32 KiB bulk reduce.
 __host__ __device__ __forceinline__ uint64_t dq_tile_base(uint64_t slice, int n_qt, int qt, int HD) {
     return (slice * n_qt + qt) * static_cast<uint64_t>(BQ) * HD;
 }
@@ -105,8 +109,9 @@ struct Smem {
     static constexpr int V_OFF = TILE;
     static constexpr int Q_OFF = 2 * TILE;
     static constexpr int DO_OFF = Q_OFF + STAGES * TILE;
-    static constexpr int DS_OFF = DO_OFF + STAGES * TILE;  // dS [128 keys][128 queries] bf16
-    static constexpr int ROW_OFF = DS_OFF + 2 * CHUNK;     // per stage: 128 -lse2, 128 D
+    static constexpr int DS_OFF = DO_OFF + DO_STAGES * TILE;  // dS [128 keys][128 queries] bf16
+    static constexpr int STG_OFF = DS_OFF + 2 * CHUNK;        // dQ staging: 64 columns fp32
+    static constexpr int ROW_OFF = STG_OFF + BQ * 64 * 4;     // per stage: 128 -lse2, 128 D
     static constexpr int BAR_OFF = ROW_OFF + STAGES * 1024;
     static constexpr int BYTES = BAR_OFF + 256;
     static constexpr int ALLOC = (BYTES + 1023 <= MAX_DSMEM) ? BYTES + 1023 : MAX_DSMEM;
@@ -118,9 +123,18 @@ __device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_
                  : "memory");
 }
 
-__device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
-    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
+// TMA bulk reduce-add of `bytes` of fp32 from shared memory into global memory
+// (performed in L2; no per-lane atomics on the SM).
+__device__ __forceinline__ void bulk_reduce_add_f32(float* gdst, uint32_t ssrc, uint32_t bytes) {
+    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(gdst), "r"(ssrc),
+                 "r"(bytes)
                  : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
 __device__ __forceinline__ float ex2_approx(float x) {
@@ -295,8 +309,8 @@ __global__ void __launch_bounds__(THREADS, 1) bwd_main_kernel(const __grid_const
     uint64_t* q_full = bars + 1;          // [2]
     uint64_t* q_empty = q_full + STAGES;  // [2]
     uint64_t* do_full = q_empty + STAGES;
-    uint64_t* do_empty = do_full + STAGES;
-    uint64_t* s_full = do_empty + STAGES;
+    uint64_t* do_empty = do_full + DO_STAGES;
+    uint64_t* s_full = do_empty + DO_STAGES;
     uint64_t* p_full = s_full + 1;
     uint64_t* dp_full = p_full + 1;
     uint64_t* ds_full = dp_full + 1;
@@ -313,12 +327,17 @@ __global__ void __launch_bounds__(THREADS, 1) bwd_main_kernel(const __grid_const
     const int kv0 = kt * BKV;
     const int n_qt = p.n_qt;
     constexpr int NCH = HD / 64;
+    // Query tiles are visited starting at the CTA's key-tile index, so the
+    // CTAs of one head (which run concurrently) reduce into different dQ tiles.
+    auto qtile = [&](int i) { const int t = i + kt % n_qt; return t >= n_qt ? t - n_qt : t; };
 
     if (warp == 0 && lane == 0) {
         mbar_init(smem_u32(kv_full), 1);
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(smem_u32(&q_full[s]), 1);
             mbar_init(smem_u32(&q_empty[s]), 1);
+        }
+        for (int s = 0; s < DO_STAGES; ++s) {
             mbar_init(smem_u32(&do_full[s]), 1);
             mbar_init(smem_u32(&do_empty[s]), 1);
         }
@@ -360,16 +379,17 @@ __global__ void __launch_bounds__(THREADS, 1) bwd_main_kernel(const __grid_const
                 const uint32_t qb = smem_u32(&q_full[st]);
                 mbar_arrive_expect_tx(qb, SM::TILE + 1024);
                 for (int c = 0; c < NCH; ++c)
-                    tma_load_4d(smem_u32(sQ + st * SM::TILE + c * SM::CHUNK), &tmQ, qb, c * 64, i * BQ, hh, bb);
-                bulk_load(smem_u32(smem + SM::ROW_OFF + st * 1024), rows + i * (2 * BQ), 1024, qb);
+                    tma_load_4d(smem_u32(sQ + st * SM::TILE + c * SM::CHUNK), &tmQ, qb, c * 64, qtile(i) * BQ, hh, bb);
+                bulk_load(smem_u32(smem + SM::ROW_OFF + st * 1024), rows + qtile(i) * (2 * BQ), 1024, qb);
             }
             __syncwarp();
-            mbar_wait(smem_u32(&do_empty[st]), ph ^ 1);
+            const int dst = i % DO_STAGES;
+            mbar_wait(smem_u32(&do_empty[dst]), ((i / DO_STAGES) & 1) ^ 1);
             if (elect_one()) {
-                const uint32_t db = smem_u32(&do_full[st]);
+                const uint32_t db = smem_u32(&do_full[dst]);
                 mbar_arrive_expect_tx(db, SM::TILE);
                 for (int c = 0; c < NCH; ++c)
-                    tma_load_4d(smem_u32(sdO + st * SM::TILE + c * SM::CHUNK), &tmdO, db, c * 64, i * BQ, hh, bb);
+                    tma_load_4d(smem_u32(sdO + dst * SM::TILE + c * SM::CHUNK), &tmdO, db, c * 64, qtile(i) * BQ, hh, bb);
             }
             __syncwarp();
         }
@@ -414,19 +434,21 @@ __global__ void __launch_bounds__(THREADS, 1) bwd_main_kernel(const __grid_const
             const int st = i & 1;
             const uint32_t ph = (i >> 1) & 1;
             const uint32_t soff = (st * SM::TILE) >> 4;
-            mbar_wait(smem_u32(&do_full[st]), ph);
+            const int dst = i % DO_STAGES;
+            const uint32_t doff = (dst * SM::TILE) >> 4;
+            mbar_wait(smem_u32(&do_full[dst]), (i / DO_STAGES) & 1);
             if (i > 0) mbar_wait(smem_u32(dq_empty), (i - 1) & 1);
             tc_fence_after();
             if (elect_one()) {
-                issue_t(tdP, v_kdesc, do_kdesc + soff);
+                issue_t(tdP, v_kdesc, do_kdesc + doff);
                 tc_commit(smem_u32(dp_full));
             }
             __syncwarp();
             mbar_wait(smem_u32(p_full), i & 1);
             tc_fence_after();
             if (elect_one()) {
-                issue_acc(tdV, tS, do_mdesc + soff, i > 0);
-                tc_commit(smem_u32(&do_empty[st]));
+                issue_acc(tdV, tS, do_mdesc + doff, i > 0);
+                tc_commit(smem_u32(&do_empty[dst]));
             }
             __syncwarp();
             if (i + 1 < n_qt) {
@@ -468,16 +490,16 @@ __global__ void __launch_bounds__(THREADS, 1) bwd_main_kernel(const __grid_const
         for (int i = 0; i < n_qt; ++i) {
             const int st = i & 1;
             const uint32_t ph = (i >> 1) & 1;
-            // keep words: bit e of kt[c] = keep(query i*128 + 64h + 32c + e, key kv0 + r)
-            uint32_t kt[2];
+            // keep words: bit e of kw[c] = keep(query i*128 + 64h + 32c + e, key kv0 + r)
+            uint32_t kw[2];
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
-                const int qrow = i * BQ + 64 * h + 32 * c + static_cast<int>(lane);
+                const int qrow = qtile(i) * BQ + 64 * h + 32 * c + static_cast<int>(lane);
                 uint32_t w = 0;
                 if (qrow < p.S) w = row_word<MODE, R>(p, (slice * p.S + qrow) * static_cast<uint64_t>(p.S) + kcol, kvalid);
-                kt[c] = transpose32(w, lane);
+                kw[c] = transpose32(w, lane);
             }
-            if (!key_valid) kt[0] = kt[1] = 0;
+            if (!key_valid) kw[0] = kw[1] = 0;
             const float* nlse = sRows + st * 256 + 64 * h;
             const float* Dv = nlse + BQ;
             mbar_wait(smem_u32(&q_full[st]), ph);  // rows of tile i landed (already complete)
@@ -502,9 +524,9 @@ __global__ void __launch_bounds__(THREADS, 1) bwd_main_kernel(const __grid_const
                     const float p2 = ex2_approx(t1.x), p3 = ex2_approx(t1.y);
                     pb[c][e / 2] = pack_bf16(p0, p1);
                     pb[c][e / 2 + 1] = pack_bf16(p2, p3);
-                    wpk[e / 2] = pack_bf16(((kt[c] >> e) & 1u) ? p0 : 0.0f, ((kt[c] >> (e + 1)) & 1u) ? p1 : 0.0f);
+                    wpk[e / 2] = pack_bf16(((kw[c] >> e) & 1u) ? p0 : 0.0f, ((kw[c] >> (e + 1)) & 1u) ? p1 : 0.0f);
                     wpk[e / 2 + 1] =
-                        pack_bf16(((kt[c] >> (e + 2)) & 1u) ? p2 : 0.0f, ((kt[c] >> (e + 3)) & 1u) ? p3 : 0.0f);
+                        pack_bf16(((kw[c] >> (e + 2)) & 1u) ? p2 : 0.0f, ((kw[c] >> (e + 3)) & 1u) ? p3 : 0.0f);
                 }
                 tmem_st16(tS + 16 * c, wpk);
             }
@@ -514,7 +536,7 @@ __global__ void __launch_bounds__(THREADS, 1) bwd_main_kernel(const __grid_const
             if (lane == 0) mbar_arrive(smem_u32(p_full));
             // ---- dS phase: dS = P o (keep ? dP/p : 0 - D) -> TMEM (bf16, for dK) and smem (for dQ)
             mbar_wait(smem_u32(dp_full), i & 1);
-            tc_fence_after();
+                    tc_fence_after();
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
                 uint32_t d[32];
@@ -530,7 +552,7 @@ __global__ void __launch_bounds__(THREADS, 1) bwd_main_kernel(const __grid_const
                     for (int u = 0; u < 4; ++u) {
                         const uint32_t pw = pb[c][(e + u) / 2];
                         const float pv = ((e + u) & 1) ? bf16_hi(pw) : bf16_lo(pw);
-                        const float dp = ((kt[c] >> (e + u)) & 1u) ? __uint_as_float(d[e + u]) * p.inv_keep : 0.0f;
+                        const float dp = ((kw[c] >> (e + u)) & 1u) ? __uint_as_float(d[e + u]) * p.inv_keep : 0.0f;
                         ds[u] = pv * (dp - dv[u]);
                     }
                     dpk[e / 2] = pack_bf16(ds[0], ds[1]);
@@ -582,29 +604,69 @@ __global__ void __launch_bounds__(THREADS, 1) bwd_main_kernel(const __grid_const
             }
         }
     } else if (warp >= 12) {  // ------------------------------------------------- dQ drain
+        // TMEM -> smem staging (64 columns, the accumulator's blocked layout)
+        // -> one 32 KiB TMA bulk reduce-add per half.  The second half is held
+        // in registers while the first is staged, so TMEM is released before
+        // the staging buffer has to be reused.
         const uint32_t qw = warp & 3;
         const int r = static_cast<int>(qw * 32 + lane);
         const uint32_t tdq = tmem + ((qw * 32) << 16) + 128;
+        float4* stg = reinterpret_cast<float4*>(smem + SM::STG_OFF);
+        const uint32_t stg_addr = smem_u32(stg);
+        const bool leader = warp == 12 && lane == 0;
+        constexpr uint32_t HALF_BYTES = BQ * 64 * 4;
+        auto stage = [&](const uint32_t (&v)[32], int c_local) {
+#pragma unroll
+            for (int g = 0; g < 8; ++g)
+                stg[(c_local * 8 + g) * BQ + r] = make_float4(__uint_as_float(v[4 * g]), __uint_as_float(v[4 * g + 1]),
+                                                             __uint_as_float(v[4 * g + 2]), __uint_as_float(v[4 * g + 3]));
+        };
+        auto flush = [&](float* gdst) {  // all 4 drain warps staged -> one bulk reduce
+            fence_proxy_async_smem();
+            named_bar_sync(1, 128);
+            if (leader) {
+                if (!(p.debug & 1)) bulk_reduce_add_f32(gdst, stg_addr, HALF_BYTES);
+                bulk_commit();
+            }
+        };
+        auto staging_free = [&]() {
+            if (leader) bulk_wait_read0();
+            named_bar_sync(1, 128);
+        };
         for (int i = 0; i < n_qt; ++i) {
             mbar_wait(smem_u32(dq_full), i & 1);
             tc_fence_after();
-            float* acc = p.dq_acc + dq_tile_base(slice, n_qt, i, HD);
-#pragma unroll 1
-            for (int c = 0; c < HD / 32; ++c) {
+            float* acc = p.dq_acc + dq_tile_base(slice, n_qt, qtile(i), HD);
+            uint32_t hi0[32], hi1[32];
+            staging_free();
+            {
                 uint32_t v[32];
-                tmem_ld32(tdq + 32 * c, v);
+                tmem_ld32(tdq, v);
                 tmem_ld_wait_regs(v);
-                if (c == HD / 32 - 1) {  // all of this warp's TMEM reads are done
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(smem_u32(dq_empty));
-                }
-#pragma unroll
-                for (int g = 0; g < 8; ++g)
-                    red_add_v4(acc + dq_off(r, 32 * c + 4 * g), __uint_as_float(v[4 * g]), __uint_as_float(v[4 * g + 1]),
-                               __uint_as_float(v[4 * g + 2]), __uint_as_float(v[4 * g + 3]));
+                stage(v, 0);
+                tmem_ld32(tdq + 32, v);
+                tmem_ld_wait_regs(v);
+                stage(v, 1);
+            }
+            if constexpr (HD == 128) {
+                tmem_ld32(tdq + 64, hi0);
+                tmem_ld32(tdq + 96, hi1);
+                tmem_ld_wait();
+                reg_fence(hi0);
+                reg_fence(hi1);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(dq_empty));  // TMEM dQ region free
+            flush(acc);
+            if constexpr (HD == 128) {
+                staging_free();
+                stage(hi0, 0);
+                stage(hi1, 1);
+                flush(acc + BQ * 64);
             }
         }
+        if (leader) bulk_wait_all();
     }
     tc_fence_before();
     __syncthreads();
@@ -685,6 +747,7 @@ cudaError_t launch_attn_bwd(const AttnBwdJob& j, cudaStream_t s) {
     p.dV = j.dv.ptr; p.v_sb = j.dv.sb; p.v_sh = j.dv.sh; p.v_ss = j.dv.ss;
     int mode = j.mode;
     if (mode == rgo_attn::MASK_PHILOX && j.threshold >= (uint64_t{1} << 32)) mode = rgo_attn::MASK_NONE;
+    if (const char* dbg = getenv("RGO_BWD_DEBUG")) p.debug = atoi(dbg);
     cudaError_t e = cudaErrorInvalidValue;
 #define RGO_B(HDV, MODEV, RV) \
     if (j.HD == HDV && mode == MODEV) { e = launch_main<HDV, MODEV, RV>(tq, tk, tv, tdo, p, s); goto launched; }

@@ -24,6 +24,21 @@ elif which.startswith("attn"):
         dict(mask_source=2, keep_prob=0.9, seed=42, rounds=10)
     for _ in range(3):
         rgo.attn_fwd(q, k, v, o, **kw)
+elif which.startswith("bwd"):
+    B, H, S, D = 4, 32, 4096, 128
+    qkv = (torch.rand(B * S, 3 * H * D, device="cuda") * 2 - 1).bfloat16()
+    v4 = qkv.view(B, S, 3, H, D)
+    q, k, v = (v4[:, :, i].permute(0, 2, 1, 3) for i in range(3))
+    o = torch.empty(B, S, H, D, dtype=torch.bfloat16, device="cuda").permute(0, 2, 1, 3)
+    do = (torch.rand(B, S, H, D, device="cuda") * 2 - 1).bfloat16().permute(0, 2, 1, 3)
+    lse = torch.empty(B * H * S, device="cuda")
+    bits = rgo.generate_mask_device(rgo.MaskLayout(B, H, S, 42), rgo.KeepThreshold(0.9), 10)
+    kw = {"bwd_bits": dict(mask_source=1, keep_prob=0.9, bits=bits),
+          "bwd_philox": dict(mask_source=2, keep_prob=0.9, seed=42, rounds=10),
+          "bwd_none": dict(mask_source=0)}[which]
+    rgo.attn_fwd(q, k, v, o, lse=lse, **kw)
+    for _ in range(3):
+        rgo.attn_bwd(q, k, v, o, do, lse, **kw)
 elif which == "mask":
     lay = rgo.MaskLayout(4, 32, 4096, 42)
     out = torch.empty(lay.elem_count() // 8, dtype=torch.uint8, device="cuda")

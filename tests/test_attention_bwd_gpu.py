@@ -14,7 +14,7 @@ import oracle
 
 pytestmark = pytest.mark.gpu
 TOL_O = 5e-3
-TOL_GRAD = 1e-2
+TOL_GRAD = 5e-3
 
 
 def rel(a, b):
