@@ -201,6 +201,138 @@ def bench_mask_kernel(rgo, cfg, rank, steps, warmup):
     return ms, elems
 
 
+def run_block_modes(rgo, wl, rank, world, args, modes):
+    """Each mode: W warm-up steps, then exactly K timed steps bracketed by
+    barrier + synchronize (CUDA events, max over ranks).  The modes are
+    measured twice, in opposite orders, and averaged, so the GPU's power /
+    clock state (the FP8 GEMMs run at the 1 kW cap) biases none of them."""
+    import torch
+    from paper_2410_07531_b200.sharding import replica_base_offset
+    base = replica_base_offset(wl.batch, wl.heads, wl.seq, rank)  # disjoint Philox counters per rank
+    weights = rgo.block.make_weights(wl, 42, torch.device("cuda"))
+    launch = {"streams": tuple(args.rng_launch), "in_gemm": (0, args.rng_warps, 0)}
+    blocks = {m: rgo.Block(wl, m, seed=42, base_offset=base, weights=weights, rng_launch=launch.get(m, (0, 0, 0)))
+              for m in modes}
+    stream = torch.cuda.current_stream()
+    samples = {m: [] for m in modes}
+    phases, launches = {}, {}
+    for order in (modes, modes[::-1]):
+        for m in order:
+            b = blocks[m]
+            for _ in range(args.warmup):
+                b.step()
+            ms, n = time_steps(b.step, args.steps, world, stream)
+            samples[m].append(max_over_ranks(ms, world))
+            phases[m] = b.last_timings()
+            launches[m] = n
+    res = {m: sum(v) / len(v) for m, v in samples.items()}
+    return blocks, res, samples, phases, launches
+
+
+def block_summary(rgo, wl, res, phases, mask_ms, peaks):
+    gemm_flops = sum(g.flops() for g in rgo.gemm_shapes(wl))
+    attn_flops = rgo.attention_work(wl)[0]
+    fp8_peak = 2 * peaks["bf16_tflops"]
+    roof_ms = gemm_flops / fp8_peak / 1e9 + attn_flops / peaks["bf16_tflops"] / 1e9
+    best = min(("streams", "in_gemm"), key=lambda m: res[m])
+    value = res[best]
+    hidden = 1.0 - (value - res["no_rng"]) / mask_ms if res.get("no_rng") else None
+    return best, value, {
+        "speedup_vs_fused": round(res["serial_fused"] / value, 4),
+        "modes_ms": {m: round(v, 4) for m, v in res.items()},
+        "phases_ms": {m: {"gemm_window": round(p[0], 4), "attention": round(p[1], 4)} for m, p in phases.items()},
+        "rng_hidden_fraction": None if hidden is None else round(hidden, 4),
+        "mask_ms": round(mask_ms, 4),
+        "block_roofline": {"ms": round(roof_ms, 4), "frac": round(roof_ms / value, 4)},
+    }
+
+
+def event_ms(fn, reps, world, warm=1):
+    import torch
+    for _ in range(warm):
+        fn()
+    ms, _ = time_steps(lambda: (fn(), 1)[1], reps, world, torch.cuda.current_stream())
+    return max_over_ranks(ms, world)
+
+
+def bench_attention_bwd(rgo, rank, world, peaks):
+    """North star (4): attention forward + backward reading the precomputed
+    bitmask vs the same kernels with Philox-10 fused in, at the Llama2-7B
+    attention shape (B4 nH32 SQ4096 dH128, token-major QKV), per rank."""
+    import torch
+    from paper_2410_07531_b200.sharding import replica_base_offset
+    B, H, S, D = L["batch"], L["heads"], L["seq"], L["head_dim"]
+    base = replica_base_offset(B, H, S, rank)
+    qkv = (torch.rand(B * S, 3 * H * D, device="cuda") * 2 - 1).bfloat16()
+    v4 = qkv.view(B, S, 3, H, D)
+    q, k, v = (v4[:, :, i].permute(0, 2, 1, 3) for i in range(3))
+    o = torch.empty(B, S, H, D, dtype=torch.bfloat16, device="cuda").permute(0, 2, 1, 3)
+    do = (torch.rand(B, S, H, D, device="cuda") * 2 - 1).bfloat16().permute(0, 2, 1, 3)
+    g = [torch.empty(B, S, H, D, dtype=torch.bfloat16, device="cuda").permute(0, 2, 1, 3) for _ in range(3)]
+    lse = torch.empty(B * H * S, dtype=torch.float32, device="cuda")
+    bits = rgo.generate_mask_device(rgo.MaskLayout(B, H, S, 42, base), rgo.KeepThreshold(L["keep_prob"]), 10)
+    a = rgo._lib.attn_desc(B, H, S, D, 0.0, 0, 1.0, 0, 0, 10, 0)
+    need = rgo._lib.C.c_uint64()
+    rgo._lib.check(rgo._lib.lib().rgo_attn_bwd_workspace(a, rgo._lib.C.byref(need)))
+    work = torch.empty(need.value, dtype=torch.uint8, device="cuda")
+    flops_f = 4 * B * H * S * S * D
+    out = {}
+    for name, kw in (("bits", dict(mask_source=1, keep_prob=L["keep_prob"], bits=bits)),
+                     ("philox_fused", dict(mask_source=2, keep_prob=L["keep_prob"], seed=42, base_offset=base,
+                                           rounds=10)),
+                     ("no_dropout", dict(mask_source=0))):
+        fwd = event_ms(lambda: rgo.attn_fwd(q, k, v, o, lse=lse, **kw), 5, world)
+        bwd = event_ms(lambda: rgo.attn_bwd(q, k, v, o, do, lse, dq=g[0], dk=g[1], dv=g[2], work=work, **kw),
+                       5, world)
+        out[name] = {"fwd_ms": round(fwd, 4), "bwd_ms": round(bwd, 4),
+                     "fwd_tflops": round(flops_f / fwd / 1e9, 1), "bwd_tflops": round(2.5 * flops_f / bwd / 1e9, 1)}
+    mask_ms = event_ms(lambda: rgo.generate_mask_device(rgo.MaskLayout(B, H, S, 42, base),
+                                                        rgo.KeepThreshold(L["keep_prob"]), 10, out=bits), 5, world)
+    out["mask_ms"] = round(mask_ms, 4)
+    out["bwd_speedup_bits_vs_fused"] = round(out["philox_fused"]["bwd_ms"] / out["bits"]["bwd_ms"], 4)
+    out["fwd_bwd_speedup_bits_vs_fused"] = round(
+        (out["philox_fused"]["fwd_ms"] + out["philox_fused"]["bwd_ms"]) / (out["bits"]["fwd_ms"] + out["bits"]["bwd_ms"]),
+        4)
+    out["bwd_roofline"] = {"bound": "tensor", "achieved": out["bits"]["bwd_tflops"], "peak": peaks["bf16_tflops"],
+                           "unit": "TFLOP/s", "frac": round(out["bits"]["bwd_tflops"] / peaks["bf16_tflops"], 4),
+                           "algorithmic": "2.5 x 4*B*nH*SQ^2*dH (5 GEMMs of the backward)"}
+    out["config"] = "B4 nH32 SQ4096 dH128 keep 0.9, Philox-10; the same mask serves forward and backward"
+    del qkv, o, do, g, work, bits
+    return out
+
+
+def bench_seq_sweep(rgo, rank, world, lens):
+    """BASELINE configs[4]: SQ sweep at the Llama2 head config (B1 nH32 dH128),
+    batch x head sharded over the ranks (rank r owns heads [r*32/n, (r+1)*32/n)
+    and that shard's Philox counter range; no collective).  Per SQ: mask
+    kernel, attention forward reading it, and the fused-Philox forward."""
+    import torch
+    from paper_2410_07531_b200.sharding import shard_slices
+    H_all, D = 32, 128
+    rows = []
+    for S in lens:
+        s0, s1, base = shard_slices(1, H_all, S, world, rank)
+        H = s1 - s0
+        q, k, v = ((torch.rand(1, H, S, D, device="cuda") * 2 - 1).bfloat16() for _ in range(3))
+        o = torch.empty_like(q)
+        lay = rgo.MaskLayout(1, H, S, 42, base)
+        bits = torch.empty(H * S * S // 8, dtype=torch.uint8, device="cuda")
+        thr = rgo.KeepThreshold(L["keep_prob"])
+        reps = 3 if S >= 16384 else 5
+        m_ms = event_ms(lambda: rgo.generate_mask_device(lay, thr, 10, out=bits), reps, world)
+        a_ms = event_ms(lambda: rgo.attn_fwd(q, k, v, o, mask_source=1, keep_prob=L["keep_prob"], bits=bits),
+                        reps, world)
+        f_ms = event_ms(lambda: rgo.attn_fwd(q, k, v, o, mask_source=2, keep_prob=L["keep_prob"], seed=42,
+                                             base_offset=base, rounds=10), reps, world)
+        rows.append({"seq": S, "mask_ms": round(m_ms, 4), "attn_bits_ms": round(a_ms, 4),
+                     "attn_fused_ms": round(f_ms, 4),
+                     "mask_gbit_s": round(H_all * S * S / (m_ms * 1e-3) / 1e9, 1),
+                     "attn_bits_tflops": round(4 * H_all * S * S * D / (a_ms * 1e-3) / 1e12, 1)})
+        del q, k, v, o, bits
+        torch.cuda.empty_cache()
+    return {"config": f"B1 nH32 dH128 keep 0.9 Philox-10, heads sharded over {world} rank(s)", "rows": rows}
+
+
 def bench_block(args, rank, world):
     import torch
     import paper_2410_07531_b200 as rgo
@@ -208,40 +340,19 @@ def bench_block(args, rank, world):
     wl = rgo.WorkloadConfig(batch=cfg["batch"], seq=cfg["seq"], heads=cfg["heads"], head_dim=cfg["head_dim"],
                             ffn_dim=cfg["ffn"], gated=True, keep_prob=cfg["keep_prob"], philox_rounds=cfg["rounds"])
     elems = cfg["batch"] * cfg["heads"] * cfg["seq"] ** 2
-    from paper_2410_07531_b200.sharding import replica_base_offset
-    base = replica_base_offset(cfg["batch"], cfg["heads"], cfg["seq"], rank)  # disjoint Philox counters per rank
-    weights = rgo.block.make_weights(wl, 42, torch.device("cuda"))
     modes = ["serial_fused", "streams", "in_gemm", "no_rng"]
-    launch = {"streams": tuple(args.rng_launch), "in_gemm": (0, args.rng_warps, 0)}
-    blocks = {m: rgo.Block(wl, m, seed=42, base_offset=base, weights=weights, rng_launch=launch.get(m, (0, 0, 0)))
-              for m in modes}
-    stream = torch.cuda.current_stream()
     peaks, src = load_peaks()
-    # Each mode: W warm-up steps, then exactly K timed steps bracketed by
-    # barrier + synchronize (CUDA events, max over ranks).  The modes are
-    # measured twice, in opposite orders, and averaged, so the GPU's power /
-    # clock state (the FP8 GEMMs run at the 1 kW cap) biases none of them.
-    samples = {m: [] for m in modes}
-    phases, launches = {}, {}
     with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
-        for order in (modes, modes[::-1]):
-            for m in order:
-                b = blocks[m]
-                for _ in range(args.warmup):
-                    b.step()
-                ms, n = time_steps(b.step, args.steps, world, stream)
-                samples[m].append(max_over_ranks(ms, world))
-                phases[m] = b.last_timings()
-                launches[m] = n
-    res = {m: sum(v) / len(v) for m, v in samples.items()}
+        blocks, res, samples, phases, launches = run_block_modes(rgo, wl, rank, world, args, modes)
     att_ms = phases["no_rng"][1]  # the mask-reading attention kernel alone, in situ
     clocks = clk.summary()
     mask_ms, _ = bench_mask_kernel(rgo, cfg, rank, max(5, args.steps // 2), 3)
     mask_ms = max_over_ranks(mask_ms, world)
+    best, value, summ = block_summary(rgo, wl, res, phases, mask_ms, peaks)
     # ----- e2e through the public API with host buffers: H2D of the block input
     # (e4m3 activations, pinned) + step + D2H of the step's result row block.
-    best = min(("streams", "in_gemm"), key=lambda m: res[m])
     b = blocks[best]
+    stream = torch.cuda.current_stream()
     x_host = b.x.view(torch.uint8).cpu().pin_memory()
     out_host = torch.empty(4096, dtype=torch.bfloat16).pin_memory()
 
@@ -257,16 +368,11 @@ def bench_block(args, rank, world):
     e2e_ms = max_over_ranks(e2e_ms, world)
     for blk in blocks.values():
         blk.close()
+    del blocks
+    torch.cuda.empty_cache()
 
-    gemm_flops = sum(g.flops() for g in rgo.gemm_shapes(wl))
     attn_flops = rgo.attention_work(wl)[0]
-    fp8_peak = 2 * peaks["bf16_tflops"]  # dense FP8 = 2x dense BF16 on B200; derived from the measured bf16
     bf16_peak = peaks["bf16_tflops"]
-    roof_ms = gemm_flops / fp8_peak / 1e9 + attn_flops / bf16_peak / 1e9
-    value = res[best]
-    hidden = None
-    if res["no_rng"] > 0:
-        hidden = 1.0 - (value - res["no_rng"]) / mask_ms
     line = {
         "metric": "llama2_block_ms", "value": round(value, 4), "unit": "ms", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(value, 4), "higher_is_better": False,
@@ -278,27 +384,54 @@ def bench_block(args, rank, world):
                    "global_batch": cfg["batch"] * world, "seq_len": cfg["seq"], "parallelism": f"replicas x{world}",
                    "overlap_mechanism": best,
                    "l2": "no flush: every step streams > 1 GB (mask 256 MiB, QKV 384 MiB) through a 126 MB L2"},
-        "speedup_vs_fused": round(res["serial_fused"] / value, 4),
-        "modes_ms": {m: round(v, 4) for m, v in res.items()},
+        "speedup_vs_fused": summ["speedup_vs_fused"],
+        "modes_ms": summ["modes_ms"],
         "modes_ms_samples": {m: [round(x, 4) for x in v] for m, v in samples.items()},
-        "phases_ms": {m: {"gemm_window": round(p[0], 4), "attention": round(p[1], 4)} for m, p in phases.items()},
-        "rng_hidden_fraction": None if hidden is None else round(hidden, 4),
+        "phases_ms": summ["phases_ms"],
+        "rng_hidden_fraction": summ["rng_hidden_fraction"],
         "mask_gbit_s": round(elems * world / (mask_ms * 1e-3) / 1e9, 2),
         "mask_ms": round(mask_ms, 4),
         "blocks_per_s": round(world * 1e3 / value, 3),
-        "block_roofline": {"ms": round(roof_ms, 4), "frac": round(roof_ms / value, 4),
-                           "def": f"sum(GEMM flop)/FP8 peak + attention flop/BF16 peak; FP8 peak = 2 x measured "
-                                  f"bf16 {bf16_peak} TF/s ({src})"},
+        "block_roofline": dict(summ["block_roofline"],
+                               **{"def": f"sum(GEMM flop)/FP8 peak + attention flop/BF16 peak; FP8 peak = 2 x "
+                                         f"measured bf16 {bf16_peak} TF/s ({src})"}),
         "roofline": {"bound": "tensor", "kernel": "attention fwd (mask bits), in situ (no-RNG step phase)",
                      "achieved": round(attn_flops / (att_ms * 1e-3) / 1e12, 2), "peak": bf16_peak,
                      "unit": "TFLOP/s", "frac": round(attn_flops / (att_ms * 1e-3) / 1e12 / bf16_peak, 4),
-                     "traffic": None,
+                     "traffic": profiled_traffic("attn_fwd_bits"),
                      "algorithmic": f"4*B*nH*SQ^2*dH = {attn_flops:.4e} flop per launch (workload.hpp:59-64)"},
         "e2e": {"value": round(e2e_ms, 4), "unit": "ms", "h2d_bytes_per_step": int(x_host.numel()),
                 "d2h_bytes_per_step": int(out_host.numel() * 2)},
         "clocks": clocks, "gpu_launches": launches[best],
     }
+    if not args.no_extras:
+        # BASELINE configs[2]: GPT-3 175B block (B1 SQ2048 nH96 d12288, GELU FFN 49152)
+        g = rgo.workload_preset("gpt3")
+        g.philox_rounds = args.rounds
+        gblocks, gres, _, gph, _ = run_block_modes(rgo, g, rank, world, args, modes)
+        for blk in gblocks.values():
+            blk.close()
+        del gblocks
+        torch.cuda.empty_cache()
+        gm = dict(L, batch=1, heads=96, seq=2048, rounds=args.rounds)
+        gmask, _ = bench_mask_kernel(rgo, gm, rank, 10, 3)
+        _, gval, gsum = block_summary(rgo, g, gres, gph, max_over_ranks(gmask, world), peaks)
+        line["gpt3_block"] = dict({"value_ms": round(gval, 4),
+                                   "config": "GPT-3 175B block FP8: B1 SQ2048 nH96 dH128 d12288, GELU FFN 49152, "
+                                             "keep 0.9, Philox-10"}, **gsum)
+        line["attention_fwd_bwd"] = bench_attention_bwd(rgo, rank, world, peaks)
+        line["seq_sweep"] = bench_seq_sweep(rgo, rank, world, (1024, 2048, 4096, 8192, 16384, 32768))
     return line
+
+
+def profiled_traffic(kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from
+    the committed ncu --set full capture (profiles/traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f).get(kernel)
+    except (OSError, ValueError):
+        return None
 
 
 def bench_mask_only(args, rank, world):
@@ -333,6 +466,8 @@ def main():
     ap.add_argument("--rng-warps", type=int, default=6, choices=[4, 6, 8],
                     help="mechanism B: RNG warps co-resident in each GEMM CTA")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the secondary configs (GPT-3 block, attention fwd+bwd, SQ sweep)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
