@@ -421,6 +421,16 @@ def bench_block(args, rank, world):
                                              "keep 0.9, Philox-10"}, **gsum)
         line["attention_fwd_bwd"] = bench_attention_bwd(rgo, rank, world, peaks)
         line["seq_sweep"] = bench_seq_sweep(rgo, rank, world, (1024, 2048, 4096, 8192, 16384, 32768))
+        # reduced-round Philox, stand-alone mask runtime ratios
+        # vs the paper's silicon (R5/R7 ~ 0.81, R3/R7 ~ 0.67; PAPER.md 5.2).
+        rr = {}
+        for R in (3, 5, 7, 10):
+            rr[R], _ = bench_mask_kernel(rgo, dict(cfg, rounds=R), rank, 10, 3)
+            rr[R] = max_over_ranks(rr[R], world)
+        line["philox_rounds"] = {"mask_ms": {f"R{R}": round(v, 4) for R, v in rr.items()},
+                                 "ratio_R5_R7": round(rr[5] / rr[7], 4), "ratio_R3_R7": round(rr[3] / rr[7], 4),
+                                 "paper_ratio_R5_R7": 0.81, "paper_ratio_R3_R7": 0.67,
+                                 "config": "K1 stand-alone, Llama2-7B mask (2^31 elements), keep 0.9"}
     return line
 
 
