@@ -7,6 +7,7 @@ from ncu_summary import KEYS
 
 SRC = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out"
 RND = sys.argv[2] if len(sys.argv) > 2 else "r01"
+NAME = sys.argv[3] if len(sys.argv) > 3 else "kernels"   # profiles/{RND}_{NAME}.md
 DST = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles")
 os.makedirs(DST, exist_ok=True)
 EXTRA = ["sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
@@ -22,7 +23,10 @@ lines = [f"# {RND}: ncu --set full, one launch per hot kernel (B200, Llama2-7B s
 for k, title in (("mask", "K1 rng_mask_kernel<10> (2^31 elements)"), ("gemm", "K2 FP8 GEMM FFN1 SwiGLU 16384x22016x4096"),
                  ("gemm_rng", "K4 FP8 GEMM FFN1 + 6 co-resident RNG warps"),
                  ("attn_bits", "K5 attention fwd, mask bits (B4 H32 S4096 D128)"),
-                 ("attn_philox", "K6 attention fwd, inline Philox-10")):
+                 ("attn_philox", "K6 attention fwd, inline Philox-10"),
+                 ("bwd_bits", "K7 attention bwd, mask bits (B4 H32 S4096 D128)"),
+                 ("bwd_philox", "K7 attention bwd, inline Philox-10 (fused baseline)"),
+                 ("bwd_none", "K7 attention bwd, no dropout")):
     p = os.path.join(SRC, f"raw_{k}.csv")
     if not os.path.exists(p):
         continue
@@ -39,9 +43,11 @@ for k, title in (("mask", "K1 rng_mask_kernel<10> (2^31 elements)"), ("gemm", "K
             lines.append(f"| {key} | {vals[i]} {units[i]} |")
     # dram traffic per launch
     try:
-        rd = float(vals[hdr.index("dram__bytes_read.sum")]); wr = float(vals[hdr.index("dram__bytes_write.sum")])
-        lines.append(f"| traffic (read+write) | {rd + wr:.1f} {units[hdr.index('dram__bytes_read.sum')]} |")
-    except ValueError:
+        scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        ir, iw = hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum")
+        tot = float(vals[ir]) * scale[units[ir]] + float(vals[iw]) * scale[units[iw]]
+        lines.append(f"| traffic (read+write) | {tot / 1e6:.1f} Mbyte |")
+    except (ValueError, KeyError):
         pass
     # top stall lines from the source page
     sp = os.path.join(SRC, f"source_{k}.csv.gz")
@@ -57,7 +63,7 @@ for k, title in (("mask", "K1 rng_mask_kernel<10> (2^31 elements)"), ("gemm", "K
         for r in top:
             lines.append(f"- {float(r[iall]) / tot * 100:5.1f}%  `{r[isrc].strip()[:90]}`")
     lines.append("")
-open(os.path.join(DST, f"{RND}_kernels.md"), "w").write("\n".join(lines) + "\n")
+open(os.path.join(DST, f"{RND}_{NAME}.md"), "w").write("\n".join(lines) + "\n")
 
 # launch list: kernel time shares over the bench's timed steps
 p = os.path.join(SRC, "launches_block.csv")
@@ -73,9 +79,11 @@ if os.path.exists(p):
         v = float(r["Metric Value"]) * (1e-3 if r["Metric Unit"] == "ns" else (1.0 if r["Metric Unit"] == "us" else 1e3))
         tot[name] += v; cnt[name] += 1
     s = sum(tot.values())
-    out = [f"# {RND}: launch list of `bench.py --steps 2 --warmup 1` under ncu (gpu__time_duration.sum)", "",
-           "All kernels of the run (4 block modes x (warm-up + timed) steps, plus the stand-alone mask",
-           "runs). Serialised, cold-cache times: use the shares.", "", "| kernel | launches | total us | share |",
+    out = [f"# {RND}: launch list of `bench.py --steps 2 --warmup 3 --no-cpu-baseline` under ncu "
+           "(gpu__time_duration.sum)", "",
+           "All kernels of the run: the Llama2-7B and GPT-3 blocks (4 modes x (warm-up + timed) steps), the",
+           "stand-alone mask runs, attention fwd+bwd (bits / fused Philox / none) and the SQ sweep.",
+           "Serialised, cold-cache times: use the shares.", "", "| kernel | launches | total us | share |",
            "|---|---|---|---|"]
     for name, v in sorted(tot.items(), key=lambda x: -x[1]):
         out.append(f"| `{name}` | {cnt[name]} | {v:.0f} | {v / s * 100:.1f}% |")

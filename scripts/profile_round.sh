@@ -4,16 +4,24 @@
 # returned gpurun_out/ stays small:
 #   launch list of a short bench run (per-launch device times, serialised)
 #   --set full of each hot kernel: mask (K1), GEMM FP8 (K2), GEMM + RNG warps (K4),
-#   attention with mask bits (K5), attention with inline Philox (K6)
+#   attention fwd with mask bits (K5) / inline Philox (K6), attention bwd (K7)
+#   with mask bits / inline Philox / no dropout
 set -u
 OUT=${1:-gpurun_out}
 KEEP=${KEEP_REPORTS:-""}
+KERNELS=${KERNELS:-"mask gemm gemm_rng attn_bits attn_philox bwd_bits bwd_philox bwd_none"}
 mkdir -p $OUT
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_block.csv \
-    python bench.py --steps 2 --warmup 1 --no-cpu-baseline > $OUT/bench_under_ncu.log 2>&1
-for k in mask gemm gemm_rng attn_bits attn_philox; do
-    timeout 400 ncu --set full --clock-control none --import-source on -k regex:"gemm_kernel|attn_fwd|rng_mask_kernel" \
-        -s 1 -c 1 -o /tmp/prof_$k python scripts/prof_kernels.py $k > $OUT/ncu_$k.log 2>&1
+if [ -z "${SKIP_LAUNCHES:-}" ]; then
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_block.csv \
+    python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $OUT/bench_under_ncu.log 2>&1
+fi
+for k in $KERNELS; do
+    case $k in
+        bwd_*) RX="bwd_main"; SKIP=1 ;;
+        *) RX="gemm_kernel|attn_fwd|rng_mask_kernel"; SKIP=1 ;;
+    esac
+    timeout 400 ncu -f --set full --clock-control none --import-source on -k regex:"$RX" \
+        -s $SKIP -c 1 -o /tmp/prof_$k python scripts/prof_kernels.py $k > $OUT/ncu_$k.log 2>&1
     ncu -i /tmp/prof_$k.ncu-rep --page raw --csv > $OUT/raw_$k.csv 2>/dev/null
     ncu -i /tmp/prof_$k.ncu-rep --page source --csv --print-source sass > $OUT/source_$k.csv 2>/dev/null
     gzip -f $OUT/source_$k.csv
