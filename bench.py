@@ -419,6 +419,19 @@ def bench_block(args, rank, world):
         line["gpt3_block"] = dict({"value_ms": round(gval, 4),
                                    "config": "GPT-3 175B block FP8: B1 SQ2048 nH96 dH128 d12288, GELU FFN 49152, "
                                              "keep 0.9, Philox-10"}, **gsum)
+        # BASELINE configs[3]: MoE block (Mixtral-8x7B-like): 8 experts top-2 SwiGLU FFN 14336
+        mo = rgo.workload_preset("moe")
+        mo.philox_rounds = args.rounds
+        mblocks, mres, _, mph, _ = run_block_modes(rgo, mo, rank, world, args, modes)
+        for blk in mblocks.values():
+            blk.close()
+        del mblocks
+        torch.cuda.empty_cache()
+        _, mval, msum = block_summary(rgo, mo, mres, mph, mask_ms, peaks)
+        line["moe_block"] = dict({"value_ms": round(mval, 4),
+                                  "config": "MoE block FP8: B4 SQ4096 nH32 dH128 d4096, 8 experts top-2 SwiGLU FFN "
+                                            "14336 (balanced synthetic routing: 4096 tokens per expert), keep 0.9, "
+                                            "Philox-10; RNG hidden under 2 + 16 expert GEMMs"}, **msum)
         line["attention_fwd_bwd"] = bench_attention_bwd(rgo, rank, world, peaks)
         line["seq_sweep"] = bench_seq_sweep(rgo, rank, world, (1024, 2048, 4096, 8192, 16384, 32768))
         # reduced-round Philox, stand-alone mask runtime ratios

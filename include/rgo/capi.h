@@ -248,6 +248,10 @@ int rgo_mask_load(const char* path, rgo_mask_desc* d, float* keep_prob, uint8_t*
  * Transformer-block step (the paper's timeline, schedule.hpp:111-136): the
  * four GEMMs between consecutive attention layers (Proj, FFN1, FFN2 of block
  * L-1 and QKV of block L, all FP8) followed by the attention of block L.
+ * MoE blocks (experts > 0) replace FFN1/FFN2 by a dispatch, the per-expert
+ * FFN1/FFN2 GEMMs and a combine; the RNG hides under all of them.  Routing is
+ * balanced and synthetic: token-expert pair p = t*top_k + j goes to expert
+ * p % experts, row p / experts of that expert's slice, gate 1/top_k.
  * Modes: SERIAL_FUSED = baseline (attention regenerates Philox inline);
  * STREAMS = mechanism A (K1 on a low-priority stream, capped grid, event join);
  * IN_GEMM = mechanism B (RNG warps co-resident in the GEMM CTAs + tail drain).
@@ -270,6 +274,8 @@ typedef struct rgo_block_desc {
     float a_qkv, a_proj, a_ffn1, a_ffn2;  /* FP8 dequant scales */
     float s_attn, s_proj, s_ffn1, s_ffn2; /* output quantisation scales */
     rgo_launch rng_launch;  /* STREAMS: mask-kernel launch shape */
+    uint32_t experts;       /* 0: dense FFN; > 0: MoE with `experts` expert FFNs of width ffn */
+    uint32_t top_k;         /* MoE: experts per token (balanced synthetic routing) */
 } rgo_block_desc;
 
 typedef struct rgo_block_buffers {
@@ -287,6 +293,8 @@ typedef struct rgo_block_buffers {
     uint64_t mask_bytes;
     unsigned long long* counter; /* IN_GEMM work-queue counter */
     float* lse;     /* optional [B*nH*S] */
+    void* xd;       /* MoE: e4m3 [M*top_k, d] dispatched expert inputs (NULL when dense) */
+    void* ye;       /* MoE: bf16 [M*top_k, d] expert outputs (NULL when dense) */
 } rgo_block_buffers;
 
 typedef struct rgo_block rgo_block;

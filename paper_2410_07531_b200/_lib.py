@@ -77,14 +77,14 @@ class block_desc(C.Structure):
         ("use_graph", C.c_uint32), ("seed", C.c_uint64), ("base_offset", C.c_uint64),
         ("a_qkv", C.c_float), ("a_proj", C.c_float), ("a_ffn1", C.c_float), ("a_ffn2", C.c_float),
         ("s_attn", C.c_float), ("s_proj", C.c_float), ("s_ffn1", C.c_float), ("s_ffn2", C.c_float),
-        ("rng_launch", launch),
+        ("rng_launch", launch), ("experts", C.c_uint32), ("top_k", C.c_uint32),
     ]
 
 
 class block_buffers(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in ("x", "wqkv", "wo", "w1", "w2", "qkv", "attn_o", "attn_o8", "y1", "h",
                                           "mask")] + [("mask_bytes", C.c_uint64), ("counter", C.c_void_p),
-                                                      ("lse", C.c_void_p)]
+                                                      ("lse", C.c_void_p), ("xd", C.c_void_p), ("ye", C.c_void_p)]
 
 
 # name -> (restype, argtypes).  Every symbol include/rgo/capi.h declares.

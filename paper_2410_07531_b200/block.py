@@ -48,7 +48,11 @@ class Block:
         self.attn_o = (_uniform(M * d, 9, seed, dev).view(M, d) * 0.1).to(bf)
         self.attn_o8 = torch.empty(M, d, dtype=f8, device=dev)
         self.y1 = torch.empty(M, d, dtype=f8, device=dev)
-        self.h = torch.empty(M, F, dtype=f8, device=dev)
+        E, k = cfg.experts, cfg.top_k
+        rows = M * k if E else M  # FFN rows: expert-sorted token copies for MoE
+        self.h = torch.empty(rows, F, dtype=f8, device=dev)
+        self.xd = torch.empty(rows, d, dtype=f8, device=dev) if E else None
+        self.ye = torch.empty(rows, d, dtype=bf, device=dev) if E else None
         elems = B * H * S * S
         self.mask = torch.zeros(elems // 8, dtype=torch.uint8, device=dev)
         self.counter = torch.zeros(1, dtype=torch.int64, device=dev)
@@ -65,12 +69,14 @@ class Block:
         desc.a_ffn1, desc.a_ffn2 = ku / math.sqrt(d), ku / math.sqrt(F)
         desc.s_attn, desc.s_proj, desc.s_ffn1, desc.s_ffn2 = 8.0, 1.0, 2.0, 1.0
         desc.rng_launch = _lib.launch(*rng_launch, 0)
+        desc.experts, desc.top_k = (E, k) if E else (0, 0)
         self.desc = desc
         w = weights
         bufs = _lib.block_buffers(self.x.data_ptr(), w["wqkv"].data_ptr(), w["wo"].data_ptr(), w["w1"].data_ptr(),
                                   w["w2"].data_ptr(), self.qkv.data_ptr(), self.attn_o.data_ptr(),
                                   self.attn_o8.data_ptr(), self.y1.data_ptr(), self.h.data_ptr(),
-                                  self.mask.data_ptr(), self.mask.numel(), self.counter.data_ptr(), None)
+                                  self.mask.data_ptr(), self.mask.numel(), self.counter.data_ptr(), None,
+                                  self.xd.data_ptr() if E else None, self.ye.data_ptr() if E else None)
         self._bufs = bufs
         handle = C.c_void_p()
         torch.cuda.synchronize()
@@ -106,10 +112,11 @@ def make_weights(cfg: WorkloadConfig, seed: int, device):
     import torch
     d, F = cfg.heads * cfg.head_dim, cfg.ffn()
     n1 = 2 * F if cfg.gated else F
+    E = max(1, cfg.experts)  # MoE: experts stacked along the output rows
     f8 = torch.float8_e4m3fn
     return {
         "wqkv": _uniform(3 * d * d, 4, seed, device).view(3 * d, d).to(f8),
         "wo": _uniform(d * d, 5, seed, device).view(d, d).to(f8),
-        "w1": _uniform(n1 * d, 6, seed, device).view(n1, d).to(f8),
-        "w2": _uniform(d * F, 7, seed, device).view(d, F).to(f8),
+        "w1": _uniform(E * n1 * d, 6, seed, device).view(E * n1, d).to(f8),
+        "w2": _uniform(E * d * F, 7, seed, device).view(E * d, F).to(f8),
     }

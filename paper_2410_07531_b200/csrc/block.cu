@@ -2,7 +2,8 @@
 //
 // One block = QKV GEMM -> attention -> Proj GEMM -> FFN1 GEMM -> FFN2 GEMM
 // (proj/include/rgo/workload.hpp:3-6, :44-52; LayerNorm/residual omitted as
-// in the reference).  A "step" is the steady-state rotation
+// in the reference); MoE blocks run dispatch -> E x (FFN1, FFN2) -> combine
+// in place of the FFN (balanced synthetic routing, BASELINE configs[3]).  A "step" is the steady-state rotation
 //     [Proj, FFN1, FFN2 of block L-1, QKV of block L]  ->  attention of block L
 // so the four GEMMs between consecutive attention layers form the window the
 // RNG hides under (schedule.hpp:111-136):
@@ -60,9 +61,64 @@ __global__ void quant_e4m3_kernel(const __nv_bfloat16* __restrict__ in, uint8_t*
     }
 }
 
+// MoE dispatch: row y1[t] -> xd[slot(t, j)] for every token-expert pair
+// p = t*k + j (expert p % E, row p / E of its slice).  16 bytes per thread.
+__global__ void moe_dispatch_kernel(const uint8_t* __restrict__ y1, uint8_t* __restrict__ xd, int M, int d, int k,
+                                    int E) {
+    const int vec = d / 16;
+    const uint64_t n = static_cast<uint64_t>(M) * k * vec;
+    const int me = M * k / E;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const int p = static_cast<int>(i / vec), c = static_cast<int>(i % vec);
+        const int t = p / k, e = p % E, r = p / E;
+        const uint4 v = *reinterpret_cast<const uint4*>(y1 + static_cast<uint64_t>(t) * d + 16 * c);
+        *reinterpret_cast<uint4*>(xd + (static_cast<uint64_t>(e) * me + r) * d + 16 * c) = v;
+    }
+}
+
+// MoE combine: x[t] = e4m3(sum_j ye[slot(t, j)] / k).  8 columns per thread.
+__global__ void moe_combine_kernel(const __nv_bfloat16* __restrict__ ye, uint8_t* __restrict__ x, int M, int d,
+                                   int k, int E) {
+    const int vec = d / 8;
+    const uint64_t n = static_cast<uint64_t>(M) * vec;
+    const int me = M * k / E;
+    const float gate = 1.0f / static_cast<float>(k);
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const int t = static_cast<int>(i / vec), c = static_cast<int>(i % vec);
+        float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int j = 0; j < k; ++j) {
+            const int p = t * k + j, e = p % E, r = p / E;
+            const uint4 v = *reinterpret_cast<const uint4*>(ye + (static_cast<uint64_t>(e) * me + r) * d + 8 * c);
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[q]));
+                acc[2 * q] += f.x;
+                acc[2 * q + 1] += f.y;
+            }
+        }
+        uint32_t o[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const __nv_fp8x2_storage_t lo = __nv_cvt_float2_to_fp8x2(
+                make_float2(acc[4 * q] * gate, acc[4 * q + 1] * gate), __NV_SATFINITE, __NV_E4M3);
+            const __nv_fp8x2_storage_t hi = __nv_cvt_float2_to_fp8x2(
+                make_float2(acc[4 * q + 2] * gate, acc[4 * q + 3] * gate), __NV_SATFINITE, __NV_E4M3);
+            o[q] = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
+        }
+        *reinterpret_cast<uint2*>(x + static_cast<uint64_t>(t) * d + 8 * c) = make_uint2(o[0], o[1]);
+    }
+}
+
 }  // namespace rgo_dev
 
 namespace rgo {
+
+static unsigned stream_grid(uint64_t items) {
+    return static_cast<unsigned>(std::min<uint64_t>((items + 255) / 256, 148 * 16));
+}
 
 cudaError_t launch_quant_e4m3(const void* in, void* out, uint64_t n, float scale, cudaStream_t s) {
     const uint64_t threads = (n + 15) / 16;
@@ -165,17 +221,46 @@ static cudaError_t enqueue_step(Block& b, int* launches) {
     g.rng_warps = rw;
     if ((e = launch_gemm(g, s)) != cudaSuccess) return e;
     ++n;
-    g = gemm(c, M, n1, d, x.y1, x.w1, x.h, c.gated ? rgo_gk::EPI_SWIGLU : rgo_gk::EPI_GELU, rgo_gk::OUT_E4M3,
-             c.a_ffn1, c.s_ffn1);
-    g.rng = rq;
-    g.rng_warps = rw;
-    if ((e = launch_gemm(g, s)) != cudaSuccess) return e;
-    ++n;
-    g = gemm(c, M, d, F, x.h, x.w2, x.x, rgo_gk::EPI_NONE, rgo_gk::OUT_E4M3, c.a_ffn2, c.s_ffn2);
-    g.rng = rq;
-    g.rng_warps = rw;
-    if ((e = launch_gemm(g, s)) != cudaSuccess) return e;
-    ++n;
+    if (c.experts > 0) {  // MoE FFN: dispatch -> per-expert FFN1/FFN2 -> combine
+        const int E = c.experts, k = c.top_k, me = M * k / E;
+        rgo_dev::moe_dispatch_kernel<<<stream_grid(static_cast<uint64_t>(M) * k * (d / 16)), 256, 0, s>>>(
+            static_cast<const uint8_t*>(x.y1), static_cast<uint8_t*>(x.xd), M, d, k, E);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        ++n;
+        for (int ex = 0; ex < E; ++ex) {
+            const uint8_t* xd = static_cast<const uint8_t*>(x.xd) + static_cast<uint64_t>(ex) * me * d;
+            uint8_t* h = static_cast<uint8_t*>(x.h) + static_cast<uint64_t>(ex) * me * F;
+            g = gemm(c, me, n1, d, xd, static_cast<const uint8_t*>(x.w1) + static_cast<uint64_t>(ex) * n1 * d, h,
+                     c.gated ? rgo_gk::EPI_SWIGLU : rgo_gk::EPI_GELU, rgo_gk::OUT_E4M3, c.a_ffn1, c.s_ffn1);
+            g.rng = rq;
+            g.rng_warps = rw;
+            if ((e = launch_gemm(g, s)) != cudaSuccess) return e;
+            ++n;
+            g = gemm(c, me, d, F, h, static_cast<const uint8_t*>(x.w2) + static_cast<uint64_t>(ex) * d * F,
+                     static_cast<__nv_bfloat16*>(x.ye) + static_cast<uint64_t>(ex) * me * d, rgo_gk::EPI_NONE,
+                     rgo_gk::OUT_BF16, c.a_ffn2, c.s_ffn2);
+            g.rng = rq;
+            g.rng_warps = rw;
+            if ((e = launch_gemm(g, s)) != cudaSuccess) return e;
+            ++n;
+        }
+        rgo_dev::moe_combine_kernel<<<stream_grid(static_cast<uint64_t>(M) * (d / 8)), 256, 0, s>>>(
+            static_cast<const __nv_bfloat16*>(x.ye), static_cast<uint8_t*>(x.x), M, d, k, E);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        ++n;
+    } else {
+        g = gemm(c, M, n1, d, x.y1, x.w1, x.h, c.gated ? rgo_gk::EPI_SWIGLU : rgo_gk::EPI_GELU, rgo_gk::OUT_E4M3,
+                 c.a_ffn1, c.s_ffn1);
+        g.rng = rq;
+        g.rng_warps = rw;
+        if ((e = launch_gemm(g, s)) != cudaSuccess) return e;
+        ++n;
+        g = gemm(c, M, d, F, x.h, x.w2, x.x, rgo_gk::EPI_NONE, rgo_gk::OUT_E4M3, c.a_ffn2, c.s_ffn2);
+        g.rng = rq;
+        g.rng_warps = rw;
+        if ((e = launch_gemm(g, s)) != cudaSuccess) return e;
+        ++n;
+    }
     g = gemm(c, M, 3 * d, d, x.x, x.wqkv, x.qkv, rgo_gk::EPI_NONE, rgo_gk::OUT_BF16, c.a_qkv, 1.0f);
     g.rng = rq;
     g.rng_warps = rw;

@@ -20,6 +20,9 @@ struct BlockConfig {
     float s_attn, s_proj, s_ffn1, s_ffn2;
     // mechanism A launch shape of the mask kernel (0 = auto)
     unsigned rng_grid, rng_block, rng_smem;
+    // MoE FFN (experts > 0): `experts` expert FFNs of width ffn, top_k experts
+    // per token, balanced synthetic routing (see moe_slot)
+    int experts, top_k;
 };
 
 struct BlockBuffers {
@@ -37,6 +40,8 @@ struct BlockBuffers {
     uint64_t mask_bytes;
     unsigned long long* counter;  // mask work-queue counter (IN_GEMM)
     float* lse;     // optional [B*nH*S]
+    void* xd;       // MoE: e4m3 [M*top_k, d] expert-sorted (dispatched) FFN inputs
+    void* ye;       // MoE: bf16 [M*top_k, d] expert FFN outputs before the combine
 };
 
 struct Block;

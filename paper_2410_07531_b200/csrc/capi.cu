@@ -452,6 +452,13 @@ int rgo_block_create(const rgo_block_desc* d, const rgo_block_buffers* b, int32_
     if (dm % 256 || d->ffn % 128 || (static_cast<uint64_t>(d->batch) * d->seq) % 128 || d->seq % 128)
         return fail(RGO_EINVAL, "rgo_block_create: needs d %% 256, ffn %% 128, seq %% 128 == 0");
     if (d->gated && d->ffn % 128) return fail(RGO_EINVAL, "rgo_block_create: gated ffn %% 128");
+    if (d->experts) {
+        const uint64_t pairs = static_cast<uint64_t>(d->batch) * d->seq * d->top_k;
+        if (d->top_k < 1 || d->top_k > d->experts || pairs % d->experts || (pairs / d->experts) % 128)
+            return fail(RGO_EINVAL, "rgo_block_create: MoE needs 1 <= top_k <= experts and "
+                                    "(batch*seq*top_k/experts) %% 128 == 0");
+        if (!b->xd || !b->ye) return fail(RGO_EINVAL, "rgo_block_create: MoE needs the xd and ye buffers");
+    }
     const uint64_t n = static_cast<uint64_t>(d->batch) * d->heads * d->seq * static_cast<uint64_t>(d->seq);
     if (!b->mask || b->mask_bytes < n / 8 || !b->counter || !b->x || !b->wqkv || !b->wo || !b->w1 || !b->w2 ||
         !b->qkv || !b->attn_o || !b->attn_o8 || !b->y1 || !b->h)
@@ -470,8 +477,10 @@ int rgo_block_create(const rgo_block_desc* d, const rgo_block_buffers* b, int32_
     c.a_qkv = d->a_qkv; c.a_proj = d->a_proj; c.a_ffn1 = d->a_ffn1; c.a_ffn2 = d->a_ffn2;
     c.s_attn = d->s_attn; c.s_proj = d->s_proj; c.s_ffn1 = d->s_ffn1; c.s_ffn2 = d->s_ffn2;
     c.rng_grid = d->rng_launch.grid; c.rng_block = d->rng_launch.block; c.rng_smem = d->rng_launch.dyn_smem;
+    c.experts = static_cast<int>(d->experts);
+    c.top_k = static_cast<int>(d->top_k);
     rgo::BlockBuffers bb{b->x, b->wqkv, b->wo, b->w1, b->w2, b->qkv, b->attn_o, b->attn_o8, b->y1, b->h,
-                         b->mask, b->mask_bytes, b->counter, b->lse};
+                         b->mask, b->mask_bytes, b->counter, b->lse, b->xd, b->ye};
     rgo::Block* impl = nullptr;
     cudaError_t ce = rgo::block_create(c, bb, mode, d->use_graph != 0, &impl);
     if (ce != cudaSuccess) return cuda_fail(ce, "rgo_block_create");

@@ -26,6 +26,8 @@ class WorkloadConfig:  # workload.hpp:14-35 (+ ffn_dim / gated for Llama2-7B's 1
     philox_rounds: int = 7
     ffn_dim: int = 0        # 0 = ffn_factor * hidden (reference formula)
     gated: bool = False     # SwiGLU: FFN1 has 2*ffn_dim outputs
+    experts: int = 0        # MoE: number of expert FFNs (0 = dense FFN)
+    top_k: int = 2          # MoE: experts per token
 
     def hidden(self) -> int:
         return self.heads * self.head_dim
@@ -57,8 +59,13 @@ def gemm_shapes(cfg: WorkloadConfig) -> List[GemmShape]:
     """workload.hpp:44-52; with gated=True FFN1 is the fused gate+up GEMM."""
     cfg.validate()
     rows, h, f = cfg.batch * cfg.seq, cfg.hidden(), cfg.ffn()
-    return [GemmShape("QKV", rows, 3 * h, h), GemmShape("Proj", rows, h, h),
-            GemmShape("FFN1", rows, (2 if cfg.gated else 1) * f, h), GemmShape("FFN2", rows, h, f)]
+    out = [GemmShape("QKV", rows, 3 * h, h), GemmShape("Proj", rows, h, h)]
+    if cfg.experts:  # MoE: each expert sees rows*top_k/experts tokens (balanced routing)
+        me = rows * cfg.top_k // cfg.experts
+        for e in range(cfg.experts):
+            out += [GemmShape(f"FFN1.e{e}", me, (2 if cfg.gated else 1) * f, h), GemmShape(f"FFN2.e{e}", me, h, f)]
+        return out
+    return out + [GemmShape("FFN1", rows, (2 if cfg.gated else 1) * f, h), GemmShape("FFN2", rows, h, f)]
 
 
 def attention_work(cfg: WorkloadConfig):
@@ -80,10 +87,13 @@ def workload_preset(name: str) -> WorkloadConfig:
         return WorkloadConfig(seq=2048, heads=96)
     if name == "llama2":
         return WorkloadConfig(seq=4096, heads=64)
+    if name == "moe":  # BASELINE configs[3]; shape chosen per SURVEY 8(d): Mixtral-8x7B-like
+        return WorkloadConfig(batch=4, seq=4096, heads=32, head_dim=128, ffn_dim=14336, gated=True,
+                              keep_prob=0.9, philox_rounds=10, experts=8, top_k=2)
     if name == "llama2_7b":
         return WorkloadConfig(batch=4, seq=4096, heads=32, head_dim=128, ffn_dim=11008, gated=True,
                               keep_prob=0.9, philox_rounds=10)
-    raise ValueError(f"unknown workload preset '{name}' (known: gpt3, llama2, llama2_7b)")
+    raise ValueError(f"unknown workload preset '{name}' (known: gpt3, llama2, llama2_7b, moe)")
 
 
 def _dt(t) -> int:

@@ -91,3 +91,53 @@ def test_graph_replay_is_deterministic(rgo, cuda):
         assert torch.equal(getattr(b1, k).view(torch.uint8), getattr(b2, k).view(torch.uint8)), k
     b1.close()
     b2.close()
+
+
+def moe_cfg(rgo):
+    return rgo.WorkloadConfig(batch=2, seq=256, heads=4, head_dim=128, ffn_dim=256, gated=True, keep_prob=0.9,
+                              philox_rounds=10, experts=4, top_k=2)
+
+
+def test_moe_modes_bitwise_identical(rgo, cuda):
+    import torch
+    cfg = moe_cfg(rgo)
+    outs = {}
+    for mode in ("serial_fused", "streams", "in_gemm"):
+        b = rgo.Block(cfg, mode, seed=11)
+        b.step()
+        torch.cuda.synchronize()
+        outs[mode] = {k: getattr(b, k).clone() for k in ("x", "qkv", "attn_o", "xd", "ye", "h")}
+        b.close()
+    for mode in ("streams", "in_gemm"):
+        for k, v in outs[mode].items():
+            assert torch.equal(v.view(torch.uint8), outs["serial_fused"][k].view(torch.uint8)), (mode, k)
+
+
+def test_moe_stages_vs_torch(rgo, cuda):
+    """Dispatch (balanced routing: pair p = t*k + j -> expert p % E, row p / E),
+    per-expert FFN1 (SwiGLU) / FFN2, combine (mean of the top-k outputs)."""
+    import torch
+    import torch.nn.functional as F
+    cfg = moe_cfg(rgo)
+    b = rgo.Block(cfg, "streams", seed=5)
+    b.step()
+    torch.cuda.synchronize()
+    E, k, M, d, Fd = cfg.experts, cfg.top_k, b.M, b.d, b.F
+    me = M * k // E
+    n1 = 2 * Fd
+    f8 = torch.float8_e4m3fn
+    dq, w = b.desc, b.weights
+    p = torch.arange(M * k, device="cuda")
+    slot = (p % E) * me + p // E
+    assert torch.equal(b.xd.view(torch.uint8)[slot], b.y1.view(torch.uint8)[p // k])
+    for e in range(E):
+        xe = b.xd[e * me:(e + 1) * me].float()
+        hh = (xe @ w["w1"][e * n1:(e + 1) * n1].float().T) * dq.a_ffn1
+        hh = hh.view(me, -1, 2, 128)
+        hact = (F.silu(hh[:, :, 0]) * hh[:, :, 1] * dq.s_ffn1).reshape(me, Fd)
+        assert rel(b.h[e * me:(e + 1) * me].float(), hact.to(f8).float()) < 2e-2
+        ye = (b.h[e * me:(e + 1) * me].float() @ w["w2"][e * d:(e + 1) * d].float().T) * dq.a_ffn2 * dq.s_ffn2
+        assert rel(b.ye[e * me:(e + 1) * me].float(), ye) < 5e-3
+    comb = b.ye.float()[slot].view(M, k, d).sum(1) / k
+    assert rel(b.x.float(), comb.to(f8).float()) < 2e-2
+    b.close()
