@@ -276,6 +276,10 @@ typedef struct rgo_block_desc {
     rgo_launch rng_launch;  /* STREAMS: mask-kernel launch shape */
     uint32_t experts;       /* 0: dense FFN; > 0: MoE with `experts` expert FFNs of width ffn */
     uint32_t top_k;         /* MoE: experts per token (balanced synthetic routing) */
+    uint32_t chunks;        /* > 1: pipeline the step over `chunks` batch groups (dense FFN, modes
+                               SERIAL_FUSED / STREAMS / NO_RNG); the mask buffer is then a 2-slot
+                               ring of chunk masks (schedule.hpp:206-239, capacity.hpp:51-59) */
+    uint32_t reserved2;
 } rgo_block_desc;
 
 typedef struct rgo_block_buffers {

@@ -78,6 +78,7 @@ class block_desc(C.Structure):
         ("a_qkv", C.c_float), ("a_proj", C.c_float), ("a_ffn1", C.c_float), ("a_ffn2", C.c_float),
         ("s_attn", C.c_float), ("s_proj", C.c_float), ("s_ffn1", C.c_float), ("s_ffn2", C.c_float),
         ("rng_launch", launch), ("experts", C.c_uint32), ("top_k", C.c_uint32),
+        ("chunks", C.c_uint32), ("reserved2", C.c_uint32),
     ]
 
 

@@ -30,7 +30,9 @@ class Block:
     """Owns the device buffers of one block replica and the C-ABI handle."""
 
     def __init__(self, cfg: WorkloadConfig, mode: str = "streams", seed: int = 42, base_offset: int = 0,
-                 rng_launch=(0, 0, 0), use_graph: bool = True, device="cuda", weights=None):
+                 rng_launch=(0, 0, 0), use_graph: bool = True, device="cuda", weights=None, chunks: int = 1):
+        """chunks > 1: pipeline the step over `chunks` batch groups (schedule.hpp:206-239);
+        the mask buffer is then a 2-slot ring of chunk masks."""
         import torch
         self.cfg, self.mode = cfg, mode
         B, S, H, D = cfg.batch, cfg.seq, cfg.heads, cfg.head_dim
@@ -54,7 +56,9 @@ class Block:
         self.xd = torch.empty(rows, d, dtype=f8, device=dev) if E else None
         self.ye = torch.empty(rows, d, dtype=bf, device=dev) if E else None
         elems = B * H * S * S
-        self.mask = torch.zeros(elems // 8, dtype=torch.uint8, device=dev)
+        self.chunks = max(1, chunks)
+        live = elems if self.chunks == 1 else 2 * (elems // self.chunks)
+        self.mask = torch.zeros(live // 8, dtype=torch.uint8, device=dev)
         self.counter = torch.zeros(1, dtype=torch.int64, device=dev)
         self.lse = None
         ku = 3.0  # E[(U(-1,1))^2] = 1/3 -> alpha = 3/sqrt(K) gives unit-variance outputs
@@ -70,6 +74,7 @@ class Block:
         desc.s_attn, desc.s_proj, desc.s_ffn1, desc.s_ffn2 = 8.0, 1.0, 2.0, 1.0
         desc.rng_launch = _lib.launch(*rng_launch, 0)
         desc.experts, desc.top_k = (E, k) if E else (0, 0)
+        desc.chunks = self.chunks
         self.desc = desc
         w = weights
         bufs = _lib.block_buffers(self.x.data_ptr(), w["wqkv"].data_ptr(), w["wo"].data_ptr(), w["w1"].data_ptr(),

@@ -140,6 +140,9 @@ struct Block {
     cudaEvent_t ev_fork = nullptr, ev_rng = nullptr;  // fork/join inside a step
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;    // ordering against the caller's stream
     cudaEvent_t ev_t[3] = {nullptr, nullptr, nullptr}; // phase timing (recorded inside the graph)
+    // chunked pipeline: per chunk "mask c ready" (s_rng) and "slot of c free" (s_main)
+    static constexpr int MAX_CHUNKS = 64;
+    cudaEvent_t ev_chunk[MAX_CHUNKS] = {}, ev_slot[MAX_CHUNKS] = {};
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     int launches_per_step = 0;
@@ -299,6 +302,106 @@ static cudaError_t enqueue_step(Block& b, int* launches) {
     return cudaSuccess;
 }
 
+// Chunked step (chunks > 1): the batch is split into `chunks` groups of Bc
+// items.  Stage c = quant + Proj/FFN1/FFN2/QKV on the group's M/chunks rows
+// and the attention of the group; in STREAMS mode the group's mask (the
+// contiguous slices [c*Bc*H, (c+1)*Bc*H) of the full layout, counter base
+// base_offset + c*Bc*H*S^2/4) is generated on the low-priority stream into
+// ring slot c % 2 while the group's GEMMs run, so at most two chunk masks are
+// live (one being read by attention(c-1)'s tail, one being written).
+// Results are bitwise those of the unchunked step (row-tiled GEMMs and
+// per-slice attention do not depend on the grouping).
+static cudaError_t enqueue_step_chunked(Block& b, int* launches) {
+    const BlockConfig& c = b.cfg;
+    const BlockBuffers& x = b.buf;
+    const int C = c.chunks, Bc = c.batch / C;
+    const int M = c.batch * c.seq, Mc = Bc * c.seq, d = c.heads * c.head_dim, F = c.ffn;
+    const int n1 = c.gated ? 2 * F : F;
+    const uint64_t chunk_elems = static_cast<uint64_t>(Bc) * c.heads * c.seq * static_cast<uint64_t>(c.seq);
+    const uint64_t chunk_bytes = chunk_elems / 8;
+    cudaStream_t s = b.s_main;
+    int n = 0;
+    cudaError_t e;
+    (void)M;
+    if ((e = record_timing(b, 0, s)) != cudaSuccess) return e;
+    if (b.mode == BLOCK_STREAMS) {
+        if ((e = cudaEventRecord(b.ev_fork, s)) != cudaSuccess) return e;
+        if ((e = cudaStreamWaitEvent(b.s_rng, b.ev_fork, 0)) != cudaSuccess) return e;
+    }
+    auto rows8 = [&](const void* base, int row, int ld) {
+        return static_cast<const uint8_t*>(base) + static_cast<uint64_t>(row) * ld;
+    };
+    for (int ch = 0; ch < C; ++ch) {
+        const int slot = ch & 1;
+        uint8_t* bits = x.mask + slot * chunk_bytes;
+        const uint64_t base = c.base_offset + static_cast<uint64_t>(ch) * (chunk_elems / 4);
+        if (b.mode == BLOCK_STREAMS) {
+            // mask of chunk ch starts when attention(ch-1) ends: it overlaps the
+            // chunk's GEMMs only (sharing SMs with the MUFU-bound attention
+            // slows both), and slot ch % 2 (last read by attention(ch-2)) is free
+            if (ch >= 1 && (e = cudaStreamWaitEvent(b.s_rng, b.ev_slot[ch - 1], 0)) != cudaSuccess) return e;
+            MaskJob mj{bits, chunk_elems, c.seed, base, c.threshold, c.rounds};
+            LaunchShape ls;
+            ls.grid = c.rng_grid ? c.rng_grid : static_cast<unsigned>(num_sms());
+            ls.block = c.rng_block ? c.rng_block : 256;
+            ls.dyn_smem = c.rng_smem;
+            if ((e = launch_mask(mj, ls, b.s_rng)) != cudaSuccess) return e;
+            ++n;
+            if ((e = cudaEventRecord(b.ev_chunk[ch], b.s_rng)) != cudaSuccess) return e;
+        }
+        const int r0 = ch * Mc;
+        const uint8_t* ao = static_cast<const uint8_t*>(x.attn_o) + static_cast<uint64_t>(r0) * d * 2;
+        uint8_t* ao8 = static_cast<uint8_t*>(x.attn_o8) + static_cast<uint64_t>(r0) * d;
+        if ((e = launch_quant_e4m3(ao, ao8, static_cast<uint64_t>(Mc) * d, c.s_attn, s)) != cudaSuccess) return e;
+        ++n;
+        GemmJob g;
+        g = gemm(c, Mc, d, d, ao8, x.wo, const_cast<uint8_t*>(rows8(x.y1, r0, d)), rgo_gk::EPI_NONE, rgo_gk::OUT_E4M3,
+                 c.a_proj, c.s_proj);
+        if ((e = launch_gemm(g, s)) != cudaSuccess) return e;
+        ++n;
+        g = gemm(c, Mc, n1, d, rows8(x.y1, r0, d), x.w1, const_cast<uint8_t*>(rows8(x.h, r0, F)),
+                 c.gated ? rgo_gk::EPI_SWIGLU : rgo_gk::EPI_GELU, rgo_gk::OUT_E4M3, c.a_ffn1, c.s_ffn1);
+        if ((e = launch_gemm(g, s)) != cudaSuccess) return e;
+        ++n;
+        g = gemm(c, Mc, d, F, rows8(x.h, r0, F), x.w2, const_cast<uint8_t*>(rows8(x.x, r0, d)), rgo_gk::EPI_NONE,
+                 rgo_gk::OUT_E4M3, c.a_ffn2, c.s_ffn2);
+        if ((e = launch_gemm(g, s)) != cudaSuccess) return e;
+        ++n;
+        void* qkv_c = static_cast<uint8_t*>(x.qkv) + static_cast<uint64_t>(r0) * 3 * d * 2;
+        g = gemm(c, Mc, 3 * d, d, rows8(x.x, r0, d), x.wqkv, qkv_c, rgo_gk::EPI_NONE, rgo_gk::OUT_BF16, c.a_qkv, 1.0f);
+        if ((e = launch_gemm(g, s)) != cudaSuccess) return e;
+        ++n;
+        if (ch == C - 1 && (e = record_timing(b, 1, s)) != cudaSuccess) return e;
+        if (b.mode == BLOCK_STREAMS && (e = cudaStreamWaitEvent(s, b.ev_chunk[ch], 0)) != cudaSuccess) return e;
+        AttnJob a{};
+        a.B = Bc; a.H = c.heads; a.S = c.seq; a.HD = c.head_dim;
+        a.scale = 1.0f / sqrtf(static_cast<float>(c.head_dim));
+        const long long ld = 3LL * d;
+        const __nv_bfloat16* qkv = static_cast<const __nv_bfloat16*>(qkv_c);
+        a.q = {qkv, static_cast<long long>(c.seq) * ld, c.head_dim, ld};
+        a.k = {qkv + d, static_cast<long long>(c.seq) * ld, c.head_dim, ld};
+        a.v = {qkv + 2 * d, static_cast<long long>(c.seq) * ld, c.head_dim, ld};
+        a.o = {static_cast<uint8_t*>(x.attn_o) + static_cast<uint64_t>(r0) * d * 2, static_cast<long long>(c.seq) * d,
+               c.head_dim, d};
+        a.lse = x.lse ? x.lse + static_cast<uint64_t>(ch) * Bc * c.heads * c.seq : nullptr;
+        a.mode = b.mode == BLOCK_SERIAL_FUSED ? rgo_attn::MASK_PHILOX : rgo_attn::MASK_BITS;
+        a.keep_prob = c.keep_prob;
+        a.bits = bits;
+        a.bits_bytes = chunk_bytes;
+        a.seed = c.seed;
+        a.base_offset = base;
+        a.threshold = c.threshold;
+        a.rounds = c.rounds;
+        if ((e = launch_attn_fwd(a, s)) != cudaSuccess) return e;
+        ++n;
+        if (b.mode == BLOCK_STREAMS && (e = cudaEventRecord(b.ev_slot[ch], s)) != cudaSuccess) return e;
+    }
+    if (b.mode == BLOCK_STREAMS && (e = cudaStreamWaitEvent(s, b.ev_chunk[C - 1], 0)) != cudaSuccess) return e;
+    if ((e = record_timing(b, 2, s)) != cudaSuccess) return e;
+    *launches = n;
+    return cudaSuccess;
+}
+
 cudaError_t block_create(const BlockConfig& cfg, const BlockBuffers& buf, int mode, bool use_graph, Block** out) {
     Block* b = new (std::nothrow) Block();
     if (!b) return cudaErrorMemoryAllocation;
@@ -314,12 +417,18 @@ cudaError_t block_create(const BlockConfig& cfg, const BlockBuffers& buf, int mo
     for (int t = 0; t < 3 && e == cudaSuccess; ++t) e = cudaEventCreate(&b->ev_t[t]);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&b->ev_in, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&b->ev_out, cudaEventDisableTiming);
+    if (cfg.chunks > Block::MAX_CHUNKS) e = cudaErrorInvalidValue;
+    for (int t = 0; t < cfg.chunks && cfg.chunks > 1 && e == cudaSuccess; ++t) {
+        e = cudaEventCreateWithFlags(&b->ev_chunk[t], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&b->ev_slot[t], cudaEventDisableTiming);
+    }
     if (e == cudaSuccess && use_graph) {
         // (kernel attributes and tensor maps are host-side calls, legal during capture;
         // no step is executed here, so creating a block never touches its buffers)
         e = cudaStreamBeginCapture(b->s_main, cudaStreamCaptureModeThreadLocal);
         if (e == cudaSuccess) {
-            cudaError_t e2 = enqueue_step(*b, &b->launches_per_step);
+            cudaError_t e2 = b->cfg.chunks > 1 ? enqueue_step_chunked(*b, &b->launches_per_step)
+                                               : enqueue_step(*b, &b->launches_per_step);
             e = cudaStreamEndCapture(b->s_main, &b->graph);
             if (e2 != cudaSuccess) e = e2;
         }
@@ -343,7 +452,7 @@ cudaError_t block_step(Block* b, cudaStream_t stream, int* launches) {
         e = cudaGraphLaunch(b->exec, b->s_main);
         n = b->launches_per_step;
     } else {
-        e = enqueue_step(*b, &n);
+        e = b->cfg.chunks > 1 ? enqueue_step_chunked(*b, &n) : enqueue_step(*b, &n);
     }
     if (e != cudaSuccess) return e;
     if ((e = cudaEventRecord(b->ev_out, b->s_main)) != cudaSuccess) return e;
@@ -368,6 +477,10 @@ void block_destroy(Block* b) {
         if (b->ev_t[t]) cudaEventDestroy(b->ev_t[t]);
     if (b->ev_in) cudaEventDestroy(b->ev_in);
     if (b->ev_out) cudaEventDestroy(b->ev_out);
+    for (int t = 0; t < Block::MAX_CHUNKS; ++t) {
+        if (b->ev_chunk[t]) cudaEventDestroy(b->ev_chunk[t]);
+        if (b->ev_slot[t]) cudaEventDestroy(b->ev_slot[t]);
+    }
     if (b->s_main) cudaStreamDestroy(b->s_main);
     if (b->s_rng) cudaStreamDestroy(b->s_rng);
     delete b;

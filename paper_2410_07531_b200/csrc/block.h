@@ -23,6 +23,10 @@ struct BlockConfig {
     // MoE FFN (experts > 0): `experts` expert FFNs of width ffn, top_k experts
     // per token, balanced synthetic routing (see moe_slot)
     int experts, top_k;
+    // SQ/batch-chunk pipelining (schedule.hpp:206-239): chunks > 1 splits the
+    // batch into `chunks` groups; each group's GEMMs, mask and attention form
+    // one pipeline stage and the live mask is a 2-slot ring of chunk masks
+    int chunks;
 };
 
 struct BlockBuffers {

@@ -459,7 +459,11 @@ int rgo_block_create(const rgo_block_desc* d, const rgo_block_buffers* b, int32_
                                     "(batch*seq*top_k/experts) %% 128 == 0");
         if (!b->xd || !b->ye) return fail(RGO_EINVAL, "rgo_block_create: MoE needs the xd and ye buffers");
     }
-    const uint64_t n = static_cast<uint64_t>(d->batch) * d->heads * d->seq * static_cast<uint64_t>(d->seq);
+    const uint32_t chunks = d->chunks > 1 ? d->chunks : 1;
+    if (chunks > 1 && (d->batch % chunks || d->experts || mode == RGO_OVERLAP_IN_GEMM))
+        return fail(RGO_EINVAL, "rgo_block_create: chunks must divide batch (dense FFN, not IN_GEMM)");
+    const uint64_t n_full = static_cast<uint64_t>(d->batch) * d->heads * d->seq * static_cast<uint64_t>(d->seq);
+    const uint64_t n = chunks > 1 ? 2 * (n_full / chunks) : n_full;  // chunked: 2-slot ring
     if (!b->mask || b->mask_bytes < n / 8 || !b->counter || !b->x || !b->wqkv || !b->wo || !b->w1 || !b->w2 ||
         !b->qkv || !b->attn_o || !b->attn_o8 || !b->y1 || !b->h)
         return fail(RGO_EINVAL, "rgo_block_create: missing buffer (mask needs %llu bytes)",
@@ -479,6 +483,7 @@ int rgo_block_create(const rgo_block_desc* d, const rgo_block_buffers* b, int32_
     c.rng_grid = d->rng_launch.grid; c.rng_block = d->rng_launch.block; c.rng_smem = d->rng_launch.dyn_smem;
     c.experts = static_cast<int>(d->experts);
     c.top_k = static_cast<int>(d->top_k);
+    c.chunks = static_cast<int>(chunks);
     rgo::BlockBuffers bb{b->x, b->wqkv, b->wo, b->w1, b->w2, b->qkv, b->attn_o, b->attn_o8, b->y1, b->h,
                          b->mask, b->mask_bytes, b->counter, b->lse, b->xd, b->ye};
     rgo::Block* impl = nullptr;

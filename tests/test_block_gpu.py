@@ -141,3 +141,26 @@ def test_moe_stages_vs_torch(rgo, cuda):
     comb = b.ye.float()[slot].view(M, k, d).sum(1) / k
     assert rel(b.x.float(), comb.to(f8).float()) < 2e-2
     b.close()
+
+
+@pytest.mark.parametrize("mode", ["streams", "serial_fused"])
+def test_chunked_pipeline_matches_unchunked(rgo, cuda, mode):
+    """Batch-chunk pipelining (schedule.hpp:206-239): same outputs bitwise, the
+    2-slot mask ring holds the last two chunks' masks (= slices of the full mask)."""
+    import torch
+    cfg = rgo.WorkloadConfig(batch=4, seq=256, heads=4, head_dim=128, ffn_dim=384, gated=True, keep_prob=0.9,
+                             philox_rounds=10)
+    ref = rgo.Block(cfg, mode, seed=21)
+    ref.step()
+    chk = rgo.Block(cfg, mode, seed=21, weights=ref.weights, chunks=4)
+    chk.step()
+    torch.cuda.synchronize()
+    for k in ("x", "qkv", "attn_o"):
+        assert torch.equal(getattr(chk, k).view(torch.uint8), getattr(ref, k).view(torch.uint8)), k
+    assert chk.mask.numel() == ref.mask.numel() // 2
+    if mode == "streams":
+        q = ref.mask.numel() // 4
+        assert torch.equal(chk.mask[:q], ref.mask[2 * q:3 * q])   # slot 0 = chunk 2
+        assert torch.equal(chk.mask[q:], ref.mask[3 * q:])        # slot 1 = chunk 3
+    ref.close()
+    chk.close()
