@@ -134,6 +134,32 @@ __device__ __forceinline__ float ex2_approx(float x) {
     return y;
 }
 
+// 2^x on the FMA pipes for a pair (FA4-style MUFU offload): x = n + f with
+// n = rint(x) from the 1.5*2^23 magic add, 2^f on [-0.5, 0.5] by a degree-3
+// polynomial (max rel. error 7.5e-5, far below bf16 P's 2^-9), 2^n added into
+// the exponent field.  x is clamped at -125 so masked (-inf) columns give a
+// tiny normal instead of garbage (their V rows are zero).
+__device__ __forceinline__ float2 ex2_poly2(float x0, float x1) {
+    constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
+    constexpr float c0 = 0.9999280571937561f, c1 = 0.6932610273361206f, c2 = 0.24261116981506348f,
+                    c3 = 0.05517161637544632f;
+    const float2 x = make_float2(fmaxf(x0, -125.0f), fmaxf(x1, -125.0f));
+    const float2 t = __fadd2_rn(x, make_float2(kMagic, kMagic));
+    const float2 n = __fadd2_rn(t, make_float2(-kMagic, -kMagic));
+    const float2 f = __ffma2_rn(n, make_float2(-1.0f, -1.0f), x);
+    float2 p = __ffma2_rn(make_float2(c3, c3), f, make_float2(c2, c2));
+    p = __ffma2_rn(p, f, make_float2(c1, c1));
+    p = __ffma2_rn(p, f, make_float2(c0, c0));
+    return make_float2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)),
+                       __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
+}
+// Pairs (of the 16 per 32-column chunk) whose 2^x runs on the FMA pipes: one
+// in POLY_EVERY (8: 12.5 %; 4 and 2 measured no better for the mask-bits kernel and
+// slower for the ALU-bound inline-Philox one).  MUFU.EX2 (16/clk/SM) and the tensor core need the same
+// ~1024 cycles per 128x128 tile, so shifting a share to the idle FMA pipes
+// takes the softmax off the critical path.
+constexpr int POLY_EVERY = 8;
+
 template <int HD, int MODE, int R>
 __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ,
                                                               const __grid_constant__ CUtensorMap tmK,
@@ -372,7 +398,15 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(const __grid_const
                     for (int e = 0; e < 32; e += 2) {
                         const float2 t2 = __ffma2_rn(make_float2(__uint_as_float(s[c][e]), __uint_as_float(s[c][e + 1])),
                                                      sc2, nm2);
-                        float p0 = ex2_approx(t2.x), p1 = ex2_approx(t2.y);
+                        float p0, p1;
+                        if (POLY_EVERY > 0 && (e >> 1) % POLY_EVERY == POLY_EVERY - 1) {
+                            const float2 pp = ex2_poly2(t2.x, t2.y);
+                            p0 = pp.x;
+                            p1 = pp.y;
+                        } else {
+                            p0 = ex2_approx(t2.x);
+                            p1 = ex2_approx(t2.y);
+                        }
                         rs2 = __fadd2_rn(rs2, make_float2(p0, p1));
                         if (MODE != MASK_NONE) {
                             p0 = ((kw[c] >> e) & 1u) ? p0 : 0.0f;
