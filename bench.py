@@ -391,6 +391,16 @@ def bench_block(args, rank, world):
         "rng_hidden_fraction": summ["rng_hidden_fraction"],
         "mask_gbit_s": round(elems * world / (mask_ms * 1e-3) / 1e9, 2),
         "mask_ms": round(mask_ms, 4),
+        # K1's limiter is the fma-heavy pipe: (2R-1)/4 IMAD.WIDE.U32 per element (round 1's
+        # multiply of the shared high counter word is hoisted), ~32 per clock per SM
+        # (scripts/diag/mulwide.cu); the 1-bit output is ~0.2 TB/s of HBM.
+        "rng_roofline": {"bound": "fma-heavy pipe (IMAD.WIDE.U32)",
+                         "achieved": round(elems * (2 * cfg["rounds"] - 1) / 4 / (mask_ms * 1e-3) / 1e12, 3),
+                         "peak": round(32 * 148 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12, 3),
+                         "unit": "T IMAD.WIDE/s",
+                         "frac": round(elems * (2 * cfg["rounds"] - 1) / 4 / (mask_ms * 1e-3)
+                                       / (32 * 148 * peaks.get("sm_max_mhz", 1965.0) * 1e6), 4),
+                         "hbm_write_gbs": round(elems / 8 / (mask_ms * 1e-3) / 1e9, 1)},
         "blocks_per_s": round(world * 1e3 / value, 3),
         "block_roofline": dict(summ["block_roofline"],
                                **{"def": f"sum(GEMM flop)/FP8 peak + attention flop/BF16 peak; FP8 peak = 2 x "
