@@ -673,6 +673,471 @@ __global__ void __launch_bounds__(THREADS, 1) bwd_main_kernel(const __grid_const
     if (warp == 1) tmem_dealloc<TMEM_COLS>(tmem);
 }
 
+// ============================================================================
+// K7 for head_dim 128 with 64-query tiles ("v2").  Same math and warp roles as
+// bwd_main_kernel; the smaller query tile halves the TMEM the scores need, which
+// leaves room for a double-buffered dQ^T accumulator, so the tensor core never
+// waits for the dQ drain:
+//   TMEM  S^T [0,64)  dP^T [64,128)  dQ^T x2 [128,256)  dV [256,384)  dK [384,512)
+//   S^T  = K Q^T   (M 128 keys, N 64)      dP^T = V dO^T
+//   dV  += W^T dO  (TS, K = 64 queries)    dK  += dS^T Q
+//   dQ^T = K^T dS^T (M 128 = head dims, N 64 queries, K 128 keys; both operands
+//          MN-major from smem), drained TMEM -> smem -> 32 KiB TMA bulk
+//          reduce-add, double-buffered staging.
+// ============================================================================
+constexpr int BQ2 = 64;
+
+struct Smem2 {
+    static constexpr int KCHUNK = 128 * 128;  // K/V: 128 rows x 128 B per 64-dim chunk
+    static constexpr int QCHUNK = 64 * 128;   // Q/dO: 64 rows x 128 B
+    static constexpr int KTILE = 2 * KCHUNK;
+    static constexpr int QTILE = 2 * QCHUNK;
+    static constexpr int K_OFF = 0;
+    static constexpr int V_OFF = KTILE;
+    static constexpr int Q_OFF = 2 * KTILE;
+    static constexpr int DO_OFF = Q_OFF + 2 * QTILE;
+    static constexpr int DS_OFF = DO_OFF + 2 * QTILE;       // dS [128 keys][64 queries] bf16
+    static constexpr int STG_OFF = DS_OFF + 128 * 128;      // 2 x dQ^T tile (128 x 64 fp32)
+    static constexpr int STG_BYTES = 128 * BQ2 * 4;
+    static constexpr int ROW_OFF = STG_OFF + 2 * STG_BYTES; // per stage: 64 -lse2, 64 D
+    static constexpr int BAR_OFF = ROW_OFF + 2 * 512;
+    static constexpr int BYTES = BAR_OFF + 256;
+    static constexpr int ALLOC = BYTES + 1023;
+};
+
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+
+// Accumulator of one (slice, 64-query tile): [16 query groups][128 dims][4 queries].
+__host__ __device__ __forceinline__ uint64_t dq2_tile_base(uint64_t slice, int n_qt, int qt) {
+    return (slice * n_qt + qt) * static_cast<uint64_t>(BQ2) * 128;
+}
+
+__global__ void bwd_prep2_kernel(const __nv_bfloat16* __restrict__ O, long long o_sb, long long o_sh, long long o_ss,
+                                 const __nv_bfloat16* __restrict__ dO, long long d_sb, long long d_sh, long long d_ss,
+                                 const float* __restrict__ lse, float* __restrict__ rows, int B, int H, int S,
+                                 int n_qt) {
+    const uint64_t padded = static_cast<uint64_t>(n_qt) * BQ2;
+    const uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= static_cast<uint64_t>(B) * H * padded) return;
+    const uint64_t slice = t / padded;
+    const int r = static_cast<int>(t - slice * padded);
+    const int qt = r / BQ2, rr = r % BQ2;
+    const int bb = static_cast<int>(slice / H), hh = static_cast<int>(slice % H);
+    float d = 0.0f, nl = -INFINITY;
+    if (r < S) {
+        const uint4* po = reinterpret_cast<const uint4*>(O + bb * o_sb + hh * o_sh + static_cast<long long>(r) * o_ss);
+        const uint4* pd = reinterpret_cast<const uint4*>(dO + bb * d_sb + hh * d_sh + static_cast<long long>(r) * d_ss);
+        float acc0 = 0.0f, acc1 = 0.0f;
+#pragma unroll 4
+        for (int c = 0; c < 16; ++c) {
+            const uint4 a = __ldg(po + c), b = __ldg(pd + c);
+            const uint32_t av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                acc0 = fmaf(bf16_lo(av[e]), bf16_lo(bv[e]), acc0);
+                acc1 = fmaf(bf16_hi(av[e]), bf16_hi(bv[e]), acc1);
+            }
+        }
+        d = acc0 + acc1;
+        nl = -lse[slice * S + r] * 1.4426950408889634f;
+    }
+    float* rw = rows + (slice * n_qt + qt) * (2 * BQ2);
+    rw[rr] = nl;
+    rw[BQ2 + rr] = d;
+}
+
+// thread = (slice, 64-query tile, group of 4 queries, 8 dims): 8 float4 reads
+// (128 contiguous bytes), 4 x 16-byte bf16 row writes.
+__global__ void bwd_dq2_kernel(const float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dQ, long long q_sb,
+                               long long q_sh, long long q_ss, int B, int H, int S, int n_qt, float scale) {
+    const uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t per_tile = 16 * 16;  // query groups x dim groups
+    const uint64_t total = static_cast<uint64_t>(B) * H * n_qt * per_tile;
+    if (t >= total) return;
+    const uint64_t tile = t / per_tile;  // slice * n_qt + qt
+    const int rem = static_cast<int>(t - tile * per_tile);
+    const int dg = rem % 16, qg = rem / 16;
+    const uint64_t slice = tile / n_qt;
+    const int qt = static_cast<int>(tile - slice * n_qt);
+    const float4* acc = reinterpret_cast<const float4*>(dq_acc + tile * BQ2 * 128);
+    float4 v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] = acc[qg * 128 + dg * 8 + e];
+    const int bb = static_cast<int>(slice / H), hh = static_cast<int>(slice % H);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int q = qt * BQ2 + qg * 4 + u;
+        if (q >= S) break;
+        float x[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) x[e] = (u == 0 ? v[e].x : u == 1 ? v[e].y : u == 2 ? v[e].z : v[e].w) * scale;
+        uint4 o;
+        o.x = pack_bf16(x[0], x[1]);
+        o.y = pack_bf16(x[2], x[3]);
+        o.z = pack_bf16(x[4], x[5]);
+        o.w = pack_bf16(x[6], x[7]);
+        *reinterpret_cast<uint4*>(dQ + bb * q_sb + hh * q_sh + static_cast<long long>(q) * q_ss + dg * 8) = o;
+    }
+}
+
+template <int MODE, int R>
+__global__ void __launch_bounds__(THREADS, 1) bwd_main2_kernel(const __grid_constant__ CUtensorMap tmQ,
+                                                               const __grid_constant__ CUtensorMap tmK,
+                                                               const __grid_constant__ CUtensorMap tmV,
+                                                               const __grid_constant__ CUtensorMap tmdO,
+                                                               const Params p) {
+    using SM = Smem2;
+    constexpr int HD = 128;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
+    uint8_t* smem = smem_raw + pad;
+    uint8_t* sK = smem + SM::K_OFF;
+    uint8_t* sV = smem + SM::V_OFF;
+    uint8_t* sQ = smem + SM::Q_OFF;
+    uint8_t* sdO = smem + SM::DO_OFF;
+    uint8_t* sdS = smem + SM::DS_OFF;
+    const float* sRows = reinterpret_cast<const float*>(smem + SM::ROW_OFF);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::BAR_OFF);
+    uint64_t* kv_full = bars;
+    uint64_t* q_full = bars + 1;     // [2]
+    uint64_t* q_empty = q_full + 2;  // [2]
+    uint64_t* do_full = q_empty + 2; // [2]
+    uint64_t* do_empty = do_full + 2;
+    uint64_t* s_full = do_empty + 2;
+    uint64_t* p_full = s_full + 1;
+    uint64_t* dp_full = p_full + 1;
+    uint64_t* ds_full = dp_full + 1;
+    uint64_t* dq_full = ds_full + 1;   // [2]
+    uint64_t* dq_empty = dq_full + 2;  // [2]
+    uint64_t* acc_full = dq_empty + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+
+    const uint32_t warp = warp_id(), lane = lane_id();
+    const int kt = blockIdx.x % p.n_kt;
+    const int bh = blockIdx.x / p.n_kt;
+    const int hh = bh % p.H, bb = bh / p.H;
+    const uint64_t slice = static_cast<uint64_t>(bb) * p.H + hh;
+    const int kv0 = kt * BKV;
+    const int n_qt = p.n_qt;  // 64-query tiles
+    auto qtile = [&](int i) { const int t = i + (2 * kt) % n_qt; return t >= n_qt ? t - n_qt : t; };
+
+    if (warp == 0 && lane == 0) {
+        mbar_init(smem_u32(kv_full), 1);
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(smem_u32(&q_full[s]), 1);
+            mbar_init(smem_u32(&q_empty[s]), 1);
+            mbar_init(smem_u32(&do_full[s]), 1);
+            mbar_init(smem_u32(&do_empty[s]), 1);
+            mbar_init(smem_u32(&dq_full[s]), 1);
+            mbar_init(smem_u32(&dq_empty[s]), 4);
+        }
+        mbar_init(smem_u32(s_full), 1);
+        mbar_init(smem_u32(p_full), 8);
+        mbar_init(smem_u32(dp_full), 1);
+        mbar_init(smem_u32(ds_full), 8);
+        mbar_init(smem_u32(acc_full), 1);
+        fence_mbar_init();
+        tma_prefetch_desc(&tmQ);
+        tma_prefetch_desc(&tmK);
+        tma_prefetch_desc(&tmV);
+        tma_prefetch_desc(&tmdO);
+    }
+    if (warp == 1) tmem_alloc<TMEM_COLS>(smem_u32(tmem_slot));
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {  // ------------------------------------------------------------ TMA
+        if (elect_one()) {
+            const uint32_t kb = smem_u32(kv_full);
+            mbar_arrive_expect_tx(kb, 2 * SM::KTILE);
+            for (int c = 0; c < 2; ++c) {
+                tma_load_4d(smem_u32(sK + c * SM::KCHUNK), &tmK, kb, c * 64, kv0, hh, bb);
+                tma_load_4d(smem_u32(sV + c * SM::KCHUNK), &tmV, kb, c * 64, kv0, hh, bb);
+            }
+        }
+        __syncwarp();
+        const float* rows = p.rows + slice * n_qt * (2 * BQ2);
+        for (int i = 0; i < n_qt; ++i) {
+            const int st = i & 1;
+            const uint32_t ph = (i >> 1) & 1;
+            const int qt = qtile(i);
+            mbar_wait(smem_u32(&q_empty[st]), ph ^ 1);
+            if (elect_one()) {
+                const uint32_t qb = smem_u32(&q_full[st]);
+                mbar_arrive_expect_tx(qb, SM::QTILE + 512);
+                for (int c = 0; c < 2; ++c)
+                    tma_load_4d(smem_u32(sQ + st * SM::QTILE + c * SM::QCHUNK), &tmQ, qb, c * 64, qt * BQ2, hh, bb);
+                bulk_load(smem_u32(smem + SM::ROW_OFF + st * 512), rows + qt * (2 * BQ2), 512, qb);
+            }
+            __syncwarp();
+            mbar_wait(smem_u32(&do_empty[st]), ph ^ 1);
+            if (elect_one()) {
+                const uint32_t db = smem_u32(&do_full[st]);
+                mbar_arrive_expect_tx(db, SM::QTILE);
+                for (int c = 0; c < 2; ++c)
+                    tma_load_4d(smem_u32(sdO + st * SM::QTILE + c * SM::QCHUNK), &tmdO, db, c * 64, qt * BQ2, hh, bb);
+            }
+            __syncwarp();
+        }
+    } else if (warp == 1) {  // ----------------------------------------------------- MMA
+        constexpr uint32_t IDESC_T = idesc_make(1, 1, BKV, BQ2, 0, 0);  // S^T, dP^T
+        constexpr uint32_t IDESC_ACC = idesc_make(1, 1, BKV, HD, 0, 1); // dV, dK
+        constexpr uint32_t IDESC_DQ = idesc_make(1, 1, HD, BQ2, 1, 1);  // dQ^T
+        const uint64_t k_kdesc = desc_kmajor_sw128(smem_u32(sK));
+        const uint64_t v_kdesc = desc_kmajor_sw128(smem_u32(sV));
+        const uint64_t q_kdesc = desc_kmajor_sw128(smem_u32(sQ));
+        const uint64_t do_kdesc = desc_kmajor_sw128(smem_u32(sdO));
+        const uint64_t q_mdesc = desc_sw128(smem_u32(sQ), SM::QCHUNK, 1024);
+        const uint64_t do_mdesc = desc_sw128(smem_u32(sdO), SM::QCHUNK, 1024);
+        const uint64_t k_mdesc = desc_sw128(smem_u32(sK), SM::KCHUNK, 1024);
+        const uint64_t ds_mdesc = desc_sw128(smem_u32(sdS), SM::KCHUNK, 1024);
+        const uint32_t tS = tmem, tdP = tmem + 64, tdV = tmem + 256, tdK = tmem + 384;
+        auto issue_t = [&](uint32_t d, uint64_t a, uint64_t b) {  // 128 x 64 x HD, K-major A and B
+#pragma unroll
+            for (int kk = 0; kk < HD / 16; ++kk) {
+                const uint32_t aoff = ((kk >> 2) * SM::KCHUNK + (kk & 3) * 32) >> 4;
+                const uint32_t boff = ((kk >> 2) * SM::QCHUNK + (kk & 3) * 32) >> 4;
+                mma_f16_ss(d, a + aoff, b + boff, IDESC_T, kk > 0);
+            }
+        };
+        auto issue_acc = [&](uint32_t d, uint32_t a_tmem, uint64_t b, bool acc) {  // K = 64 queries
+#pragma unroll
+            for (int kk = 0; kk < BQ2 / 16; ++kk)
+                mma_f16_ts(d, a_tmem + (kk >> 1) * 32 + (kk & 1) * 8, b + ((kk * 2048) >> 4), IDESC_ACC,
+                           (acc || kk > 0) ? 1u : 0u);
+        };
+        mbar_wait(smem_u32(kv_full), 0);
+        mbar_wait(smem_u32(&q_full[0]), 0);
+        tc_fence_after();
+        if (elect_one()) {
+            issue_t(tS, k_kdesc, q_kdesc);
+            tc_commit(smem_u32(s_full));
+        }
+        __syncwarp();
+        for (int i = 0; i < n_qt; ++i) {
+            const int st = i & 1;
+            const uint32_t ph = (i >> 1) & 1;
+            const uint32_t soff = (st * SM::QTILE) >> 4;
+            mbar_wait(smem_u32(&do_full[st]), ph);
+            tc_fence_after();
+            if (elect_one()) {
+                issue_t(tdP, v_kdesc, do_kdesc + soff);
+                tc_commit(smem_u32(dp_full));
+            }
+            __syncwarp();
+            mbar_wait(smem_u32(p_full), i & 1);
+            tc_fence_after();
+            if (elect_one()) {
+                issue_acc(tdV, tS, do_mdesc + soff, i > 0);
+                tc_commit(smem_u32(&do_empty[st]));
+            }
+            __syncwarp();
+            if (i + 1 < n_qt) {
+                const int st1 = st ^ 1;
+                mbar_wait(smem_u32(&q_full[st1]), ((i + 1) >> 1) & 1);
+                tc_fence_after();
+                if (elect_one()) {
+                    issue_t(tS, k_kdesc, q_kdesc + ((st1 * SM::QTILE) >> 4));
+                    tc_commit(smem_u32(s_full));
+                }
+                __syncwarp();
+            }
+            mbar_wait(smem_u32(ds_full), i & 1);
+            const int b = i & 1;
+            if (i >= 2) mbar_wait(smem_u32(&dq_empty[b]), ((i >> 1) - 1) & 1);
+            tc_fence_after();
+            if (elect_one()) {
+                issue_acc(tdK, tdP, q_mdesc + soff, i > 0);
+#pragma unroll
+                for (int kk = 0; kk < BKV / 16; ++kk)
+                    mma_f16_ss(tmem + 128 + 64 * b, k_mdesc + ((kk * 2048) >> 4), ds_mdesc + ((kk * 2048) >> 4),
+                               IDESC_DQ, kk > 0);
+                tc_commit(smem_u32(&q_empty[st]));
+                tc_commit(smem_u32(&dq_full[b]));
+                if (i + 1 == n_qt) tc_commit(smem_u32(acc_full));
+            }
+            __syncwarp();
+        }
+    } else if (warp >= 4 && warp < 12) {  // --------------------------------- softmax / dS
+        const int h = (warp - 4) >> 2;         // 32-query half of each 64-query tile
+        const uint32_t qw = warp & 3;
+        const int r = static_cast<int>(qw * 32 + lane);  // key row
+        const bool key_valid = kv0 + r < p.S;
+        const uint32_t lane_base = (qw * 32) << 16;
+        const uint32_t tS = tmem + lane_base + 32 * h;
+        const uint32_t tdP = tmem + lane_base + 64 + 32 * h;
+        const int kcol = kv0 + static_cast<int>(qw) * 32;
+        const int kvalid = p.S - kcol;
+        uint8_t* ds_row = sdS + r * 128;
+        const uint32_t sw = static_cast<uint32_t>(r & 7);
+        const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
+        for (int i = 0; i < n_qt; ++i) {
+            const int st = i & 1;
+            const uint32_t ph = (i >> 1) & 1;
+            const int qrow = qtile(i) * BQ2 + 32 * h + static_cast<int>(lane);
+            uint32_t w = 0;
+            if (qrow < p.S) w = row_word<MODE, R>(p, (slice * p.S + qrow) * static_cast<uint64_t>(p.S) + kcol, kvalid);
+            uint32_t kw = transpose32(w, lane);  // bit e: keep(query tile*64 + 32h + e, key kv0 + r)
+            if (!key_valid) kw = 0;
+            const float* nlse = sRows + st * 128 + 32 * h;
+            const float* Dv = nlse + BQ2;
+            mbar_wait(smem_u32(&q_full[st]), ph);  // row terms of tile i landed
+            mbar_wait(smem_u32(s_full), i & 1);
+            tc_fence_after();
+            uint32_t pb[16];
+            {
+                uint32_t s[32];
+                tmem_ld32(tS, s);
+                tmem_ld_wait_regs(s);
+                uint32_t wpk[16];
+#pragma unroll
+                for (int e = 0; e < 32; e += 4) {
+                    const float4 nl = *reinterpret_cast<const float4*>(nlse + e);
+                    const float2 t0 = __ffma2_rn(make_float2(__uint_as_float(s[e]), __uint_as_float(s[e + 1])), sc2,
+                                                 make_float2(nl.x, nl.y));
+                    const float2 t1 = __ffma2_rn(make_float2(__uint_as_float(s[e + 2]), __uint_as_float(s[e + 3])),
+                                                 sc2, make_float2(nl.z, nl.w));
+                    const float p0 = ex2_approx(t0.x), p1 = ex2_approx(t0.y);
+                    const float p2 = ex2_approx(t1.x), p3 = ex2_approx(t1.y);
+                    pb[e / 2] = pack_bf16(p0, p1);
+                    pb[e / 2 + 1] = pack_bf16(p2, p3);
+                    wpk[e / 2] = pack_bf16(((kw >> e) & 1u) ? p0 : 0.0f, ((kw >> (e + 1)) & 1u) ? p1 : 0.0f);
+                    wpk[e / 2 + 1] = pack_bf16(((kw >> (e + 2)) & 1u) ? p2 : 0.0f, ((kw >> (e + 3)) & 1u) ? p3 : 0.0f);
+                }
+                tmem_st16(tS, wpk);
+            }
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(p_full));
+            mbar_wait(smem_u32(dp_full), i & 1);
+            tc_fence_after();
+            {
+                uint32_t d[32];
+                tmem_ld32(tdP, d);
+                tmem_ld_wait_regs(d);
+                uint32_t dpk[16];
+#pragma unroll
+                for (int e = 0; e < 32; e += 4) {
+                    const float4 dd = *reinterpret_cast<const float4*>(Dv + e);
+                    const float dv[4] = {dd.x, dd.y, dd.z, dd.w};
+                    float ds[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const uint32_t pw = pb[(e + u) / 2];
+                        const float pv = ((e + u) & 1) ? bf16_hi(pw) : bf16_lo(pw);
+                        const float dp = ((kw >> (e + u)) & 1u) ? __uint_as_float(d[e + u]) * p.inv_keep : 0.0f;
+                        ds[u] = pv * (dp - dv[u]);
+                    }
+                    dpk[e / 2] = pack_bf16(ds[0], ds[1]);
+                    dpk[e / 2 + 1] = pack_bf16(ds[2], ds[3]);
+                }
+                tmem_st16(tdP, dpk);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t unit = (4 * h + u) ^ sw;
+                    *reinterpret_cast<uint4*>(ds_row + unit * 16) =
+                        make_uint4(dpk[4 * u], dpk[4 * u + 1], dpk[4 * u + 2], dpk[4 * u + 3]);
+                }
+            }
+            fence_proxy_async_smem();
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(ds_full));
+        }
+        // ---- epilogue: dV = acc / keep_prob, dK = acc * scale; dims [64h, 64h+64)
+        mbar_wait(smem_u32(acc_full), 0);
+        tc_fence_after();
+        const int key = kv0 + r;
+        __nv_bfloat16* dv_row = static_cast<__nv_bfloat16*>(p.dV) + bb * p.v_sb + hh * p.v_sh +
+                                static_cast<long long>(key_valid ? key : 0) * p.v_ss;
+        __nv_bfloat16* dk_row = static_cast<__nv_bfloat16*>(p.dK) + bb * p.k_sb + hh * p.k_sh +
+                                static_cast<long long>(key_valid ? key : 0) * p.k_ss;
+#pragma unroll 1
+        for (int which = 0; which < 2; ++which) {
+            const uint32_t tacc = tmem + lane_base + 256 + which * HD;
+            const float mul = which == 0 ? p.inv_keep : p.scale;
+            __nv_bfloat16* dst = which == 0 ? dv_row : dk_row;
+#pragma unroll 1
+            for (int c = 0; c < 2; ++c) {
+                const int col = h * 64 + 32 * c;
+                uint32_t o[32];
+                tmem_ld32(tacc + col, o);
+                tmem_ld_wait_regs(o);
+                uint32_t pk[16];
+#pragma unroll
+                for (int e = 0; e < 16; ++e)
+                    pk[e] = pack_bf16(__uint_as_float(o[2 * e]) * mul, __uint_as_float(o[2 * e + 1]) * mul);
+                if (key_valid) {
+                    uint4* d4 = reinterpret_cast<uint4*>(dst + col);
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) d4[v] = make_uint4(pk[4 * v], pk[4 * v + 1], pk[4 * v + 2], pk[4 * v + 3]);
+                }
+            }
+        }
+    } else if (warp >= 12) {  // ------------------------------------------------- dQ drain
+        // thread = head dim (TMEM lane 32*qw + lane), 64 query values per tile
+        const uint32_t qw = warp & 3;
+        const int hd = static_cast<int>(qw * 32 + lane);
+        const bool leader = warp == 12 && lane == 0;
+        for (int i = 0; i < n_qt; ++i) {
+            const int b = i & 1;
+            mbar_wait(smem_u32(&dq_full[b]), (i >> 1) & 1);
+            tc_fence_after();
+            uint32_t v0[32], v1[32];
+            const uint32_t taddr = tmem + ((qw * 32) << 16) + 128 + 64 * b;
+            tmem_ld32(taddr, v0);
+            tmem_ld32(taddr + 32, v1);
+            tmem_ld_wait();
+            reg_fence(v0);
+            reg_fence(v1);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&dq_empty[b]));  // TMEM buffer b free
+            if (leader) bulk_wait_read1();  // staging b's previous reduce (tile i-2) read out
+            named_bar_sync(1, 128);
+            float4* stg = reinterpret_cast<float4*>(smem + SM::STG_OFF + b * SM::STG_BYTES);
+#pragma unroll
+            for (int qg = 0; qg < 8; ++qg)
+                stg[qg * 128 + hd] = make_float4(__uint_as_float(v0[4 * qg]), __uint_as_float(v0[4 * qg + 1]),
+                                                 __uint_as_float(v0[4 * qg + 2]), __uint_as_float(v0[4 * qg + 3]));
+#pragma unroll
+            for (int qg = 0; qg < 8; ++qg)
+                stg[(8 + qg) * 128 + hd] = make_float4(__uint_as_float(v1[4 * qg]), __uint_as_float(v1[4 * qg + 1]),
+                                                       __uint_as_float(v1[4 * qg + 2]), __uint_as_float(v1[4 * qg + 3]));
+            fence_proxy_async_smem();
+            named_bar_sync(1, 128);
+            if (leader) {
+                if (!(p.debug & 1))
+                    bulk_reduce_add_f32(p.dq_acc + dq2_tile_base(slice, n_qt, qtile(i)), smem_u32(stg), SM::STG_BYTES);
+                bulk_commit();
+            }
+        }
+        if (leader) bulk_wait_all();
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc<TMEM_COLS>(tmem);
+}
+
+template <int MODE, int R>
+static cudaError_t launch_main2(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
+                                const CUtensorMap& dO, const Params& p, cudaStream_t s) {
+    auto kern = bwd_main2_kernel<MODE, R>;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem2::ALLOC);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    const unsigned grid = static_cast<unsigned>(p.B) * p.H * p.n_kt;
+    kern<<<grid, THREADS, Smem2::ALLOC, s>>>(q, k, v, dO, p);
+    return cudaGetLastError();
+}
+
 template <int HD, int MODE, int R>
 static cudaError_t launch_main(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
                                const CUtensorMap& dO, const Params& p, cudaStream_t s) {
@@ -698,17 +1163,78 @@ uint64_t attn_bwd_workspace_bytes(int B, int H, int S, int HD) {
     return rows * HD * 4 + rows * 2 * 4;
 }
 
-static bool tmap4(CUtensorMap* m, const AttnTensor& t, int B, int H, int S, int HD) {
+static bool tmap4(CUtensorMap* m, const AttnTensor& t, int B, int H, int S, int HD, uint32_t box_rows = 128) {
     const uint64_t dims[4] = {static_cast<uint64_t>(HD), static_cast<uint64_t>(S), static_cast<uint64_t>(H),
                               static_cast<uint64_t>(B)};
     const uint64_t strides[3] = {static_cast<uint64_t>(t.ss) * 2, static_cast<uint64_t>(t.sh) * 2,
                                  static_cast<uint64_t>(t.sb) * 2};
-    const uint32_t box[4] = {64, 128, 1, 1};
+    const uint32_t box[4] = {64, box_rows, 1, 1};
     return make_tmap(m, t.ptr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+static void fill_params(rgo_attn_bwd::Params& p, const AttnBwdJob& j, int n_qt, float* rowbuf, float* dq_acc) {
+    using namespace rgo_attn_bwd;
+    p.B = j.B; p.H = j.H; p.S = j.S;
+    p.n_qt = n_qt;
+    p.n_kt = (j.S + BKV - 1) / BKV;
+    p.scale = j.scale;
+    p.scale_log2 = j.scale * 1.4426950408889634f;
+    p.inv_keep = 1.0f / (j.mode == rgo_attn::MASK_NONE ? 1.0f : j.keep_prob);
+    p.bits = j.bits;
+    p.bits_bytes = j.bits_bytes;
+    p.bits_aligned = (j.S % 32) == 0 && (reinterpret_cast<uintptr_t>(j.bits) & 3) == 0;
+    p.k0 = static_cast<uint32_t>(j.seed);
+    p.k1 = static_cast<uint32_t>(j.seed >> 32);
+    p.base_offset = j.base_offset;
+    p.thr = static_cast<uint32_t>(j.threshold);
+    p.rounds = j.rounds;
+    p.rows = rowbuf;
+    p.dq_acc = dq_acc;
+    p.dK = j.dk.ptr; p.k_sb = j.dk.sb; p.k_sh = j.dk.sh; p.k_ss = j.dk.ss;
+    p.dV = j.dv.ptr; p.v_sb = j.dv.sb; p.v_sh = j.dv.sh; p.v_ss = j.dv.ss;
+    if (const char* dbg = getenv("RGO_BWD_DEBUG")) p.debug = atoi(dbg);
+}
+
+// head_dim 128: the 64-query-tile kernel (double-buffered dQ^T in TMEM).
+static cudaError_t launch_attn_bwd2(const AttnBwdJob& j, cudaStream_t s) {
+    using namespace rgo_attn_bwd;
+    CUtensorMap tq, tk, tv, tdo;
+    if (!tmap4(&tq, j.q, j.B, j.H, j.S, j.HD, BQ2) || !tmap4(&tk, j.k, j.B, j.H, j.S, j.HD) ||
+        !tmap4(&tv, j.v, j.B, j.H, j.S, j.HD) || !tmap4(&tdo, j.dout, j.B, j.H, j.S, j.HD, BQ2))
+        return cudaErrorInvalidResourceHandle;
+    const int n_qt = (j.S + BQ2 - 1) / BQ2;
+    const uint64_t rows = static_cast<uint64_t>(j.B) * j.H * n_qt * BQ2;
+    float* dq_acc = static_cast<float*>(j.work);
+    float* rowbuf = dq_acc + rows * j.HD;
+    cudaError_t e = cudaMemsetAsync(dq_acc, 0, rows * j.HD * sizeof(float), s);
+    if (e != cudaSuccess) return e;
+    {
+        const unsigned threads = 256;
+        const unsigned grid = static_cast<unsigned>((rows + threads - 1) / threads);
+        bwd_prep2_kernel<<<grid, threads, 0, s>>>(static_cast<const __nv_bfloat16*>(j.o.ptr), j.o.sb, j.o.sh, j.o.ss,
+                                                  static_cast<const __nv_bfloat16*>(j.dout.ptr), j.dout.sb, j.dout.sh,
+                                                  j.dout.ss, j.lse, rowbuf, j.B, j.H, j.S, n_qt);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    Params p{};
+    fill_params(p, j, n_qt, rowbuf, dq_acc);
+    int mode = j.mode;
+    if (mode == rgo_attn::MASK_PHILOX && j.threshold >= (uint64_t{1} << 32)) mode = rgo_attn::MASK_NONE;
+    if (mode == rgo_attn::MASK_NONE) e = launch_main2<rgo_attn::MASK_NONE, 0>(tq, tk, tv, tdo, p, s);
+    else if (mode == rgo_attn::MASK_BITS) e = launch_main2<rgo_attn::MASK_BITS, 0>(tq, tk, tv, tdo, p, s);
+    else if (j.rounds == 10) e = launch_main2<rgo_attn::MASK_PHILOX, 10>(tq, tk, tv, tdo, p, s);
+    else if (j.rounds == 7) e = launch_main2<rgo_attn::MASK_PHILOX, 7>(tq, tk, tv, tdo, p, s);
+    else e = launch_main2<rgo_attn::MASK_PHILOX, 0>(tq, tk, tv, tdo, p, s);
+    if (e != cudaSuccess) return e;
+    const uint64_t n = static_cast<uint64_t>(j.B) * j.H * n_qt * 256;
+    bwd_dq2_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
+        dq_acc, static_cast<__nv_bfloat16*>(j.dq.ptr), j.dq.sb, j.dq.sh, j.dq.ss, j.B, j.H, j.S, n_qt, j.scale);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_attn_bwd(const AttnBwdJob& j, cudaStream_t s) {
     using namespace rgo_attn_bwd;
+    if (j.HD == 128 && !getenv("RGO_BWD_V1")) return launch_attn_bwd2(j, s);
     CUtensorMap tq, tk, tv, tdo;
     if (!tmap4(&tq, j.q, j.B, j.H, j.S, j.HD) || !tmap4(&tk, j.k, j.B, j.H, j.S, j.HD) ||
         !tmap4(&tv, j.v, j.B, j.H, j.S, j.HD) || !tmap4(&tdo, j.dout, j.B, j.H, j.S, j.HD))

@@ -5,7 +5,7 @@ on bf16-rounded inputs.  Tolerance (north_star, BF16): relative Frobenius
 error <= 5e-3 for O and <= TOL_GRAD for dQ/dK/dV (P and dS pass through bf16
 on the tensor cores).  The decoupled (mask bits) and fused (Philox inline)
 backwards use identical keep decisions: dK, dV bitwise equal; dQ is reduced
-with fp32 atomics across key tiles (order-dependent rounding) and must agree
+with fp32 reductions across key tiles (order-dependent rounding) and must agree
 to fp32-accumulation accuracy."""
 import numpy as np
 import pytest
