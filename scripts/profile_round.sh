@@ -28,4 +28,12 @@ for k in $KERNELS; do
     if [ -n "$KEEP" ]; then cp /tmp/prof_$k.ncu-rep $OUT/; fi
     tail -1 $OUT/ncu_$k.log
 done
+# whole block steps per overlap mode, concurrency preserved (app-range replay)
+if [ -z "${SKIP_RANGE:-}" ]; then
+mkdir -p $OUT/rng_range
+for m in no_rng streams in_gemm serial_fused; do
+    timeout 300 ncu --replay-mode app-range --clock-control none --metrics gpu__time_duration.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed,sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed,smsp__issue_active.avg.pct_of_peak_sustained_elapsed,sm__cycles_elapsed.avg.per_second,dram__bytes_write.sum,sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_elapsed \
+        --csv python scripts/prof_block_range.py $m > $OUT/rng_range/$m.csv 2>&1
+done
+fi
 du -sh $OUT
