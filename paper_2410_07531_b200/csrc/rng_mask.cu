@@ -32,7 +32,7 @@ __device__ __forceinline__ void st_v4_streaming(uint8_t* p, uint32_t a, uint32_t
 
 // Vectors [0, n_vec) of the mask; vector v covers elements [128v, 128v+128).
 template <int R>
-__global__ void __launch_bounds__(256) rng_mask_kernel(uint8_t* __restrict__ out, uint64_t n_vec,
+__global__ void __launch_bounds__(256, (R == 4 || R == 5) ? 4 : 0) rng_mask_kernel(uint8_t* __restrict__ out, uint64_t n_vec,
                                                        uint64_t base_offset, uint32_t k0,
                                                        uint32_t k1, uint32_t thr, uint32_t zero) {
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;

@@ -27,9 +27,10 @@ def run(mode, launch=(0, 0, 0), steps=10):
                       "attention": round(ph[1], 4)}), flush=True)
 
 
-run("no_rng")
-run("serial_fused")
-for w in (4, 6, 8):
-    run("in_gemm", (0, w, 0))
-for launch in [(148, 128, 0)]:
-    run("streams", launch)
+configs = [("no_rng", (0, 0, 0)), ("serial_fused", (0, 0, 0)), ("in_gemm", (0, 6, 0)), ("in_gemm", (0, 8, 0)),
+           ("streams", (148, 128, 0)), ("streams", (148, 256, 0)), ("streams", (148, 64, 0)),
+           ("streams", (74, 128, 0))]
+# three passes in alternating order: the 1 kW power state drifts during a run
+for rep in range(3):
+    for mode, launch in (configs if rep % 2 == 0 else configs[::-1]):
+        run(mode, launch)
