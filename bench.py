@@ -571,7 +571,7 @@ def main():
     rank, world, _ = dist_setup()
     line = bench_block(args, rank, world) if args.workload == "block" else bench_mask_only(args, rank, world)
     if rank == 0:
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:  # the CPU baseline is an N=1 measurement
             cb = cpu_reference_block(dict(L, rounds=args.rounds))
             line["cpu_baseline"] = {k: (round(cb[k], 1) if k == "value" else cb[k])
                                     for k in ("value", "unit", "cores", "kind", "sample")}
