@@ -136,3 +136,26 @@ def test_token_major_layout_and_lse(rgo, cuda):
     sc = (qc.float() @ kc.float().transpose(-1, -2)) / np.sqrt(D)
     ref_lse = torch.logsumexp(sc, -1).reshape(-1)
     torch.testing.assert_close(lse, ref_lse, rtol=1e-3, atol=1e-3)
+
+
+@pytest.mark.parametrize("base", [(1 << 32) - 5000, (1 << 64) - 3000])
+def test_counter_carry_and_wrap_fwd_bwd(rgo, cuda, base):
+    """The Philox counter crosses a 2^32 boundary (carry into c1) or wraps 2^64
+    (element_source, mask.hpp:72-85) inside a slice: the inline-Philox forward
+    and backward (K6, K7) must still make K1's keep decisions bit for bit."""
+    import torch
+    B, H, S, D = 1, 2, 512, 128
+    g = torch.Generator(device="cpu").manual_seed(11)
+    q, k, v, do = ((torch.rand(B, H, S, D, generator=g) * 2 - 1).bfloat16().cuda() for _ in range(4))
+    bits = rgo.generate_mask_device(rgo.MaskLayout(B, H, S, 99, base), rgo.KeepThreshold(0.9), 10)
+    lse_b = torch.empty(B * H * S, device="cuda")
+    lse_f = torch.empty(B * H * S, device="cuda")
+    ob = rgo.attn_fwd(q, k, v, mask_source=1, keep_prob=0.9, bits=bits, lse=lse_b)
+    of = rgo.attn_fwd(q, k, v, mask_source=2, keep_prob=0.9, seed=99, base_offset=base, rounds=10, lse=lse_f)
+    assert torch.equal(ob, of)
+    gb = rgo.attn_bwd(q, k, v, ob, do, lse_b, mask_source=1, keep_prob=0.9, bits=bits)
+    gf = rgo.attn_bwd(q, k, v, of, do, lse_f, mask_source=2, keep_prob=0.9, seed=99, base_offset=base, rounds=10)
+    assert torch.equal(gb[1], gf[1]) and torch.equal(gb[2], gf[2])
+    # and the mask itself is the oracle's
+    want = oracle.generate_mask(B, H, S, 99, base, 0.9, 10)
+    assert np.array_equal(bits[: want.size].cpu().numpy(), want)
