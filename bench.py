@@ -29,6 +29,12 @@ sys.path.insert(0, ROOT)
 L = dict(batch=4, seq=4096, heads=32, head_dim=128, ffn=11008, keep_prob=0.9, rounds=10)
 
 
+def log(msg):
+    """Progress on stderr (the JSON line is the only stdout output)."""
+    if int(os.environ.get("RANK", "0")) == 0:
+        print(f"[bench {time.strftime('%H:%M:%S')}] {msg}", file=sys.stderr, flush=True)
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -342,8 +348,10 @@ def bench_block(args, rank, world):
     elems = cfg["batch"] * cfg["heads"] * cfg["seq"] ** 2
     modes = ["serial_fused", "streams", "in_gemm", "no_rng"]
     peaks, src = load_peaks()
+    log("Llama2-7B block modes")
     with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
         blocks, res, samples, phases, launches = run_block_modes(rgo, wl, rank, world, args, modes)
+    log("mask kernel")
     att_ms = phases["no_rng"][1]  # the mask-reading attention kernel alone, in situ
     clocks = clk.summary()
     mask_ms, _ = bench_mask_kernel(rgo, cfg, rank, max(5, args.steps // 2), 3)
@@ -355,6 +363,7 @@ def bench_block(args, rank, world):
     # reads back a row block of its result.  Two block replicas alternate so the
     # next step's 128 MiB H2D (copy stream) overlaps the current step, as a
     # serving loop would do.
+    log("e2e")
     b = blocks[best]
     stream = torch.cuda.current_stream()
     b2 = rgo.Block(wl, best, seed=42, base_offset=b.desc.base_offset, weights=b.weights,
@@ -448,6 +457,7 @@ def bench_block(args, rank, world):
     }
     if not args.no_extras:
         # BASELINE configs[2]: GPT-3 175B block (B1 SQ2048 nH96 d12288, GELU FFN 49152)
+        log("GPT-3 block")
         g = rgo.workload_preset("gpt3")
         g.philox_rounds = args.rounds
         gblocks, gres, _, gph, _ = run_block_modes(rgo, g, rank, world, args, modes)
@@ -462,6 +472,7 @@ def bench_block(args, rank, world):
                                    "config": "GPT-3 175B block FP8: B1 SQ2048 nH96 dH128 d12288, GELU FFN 49152, "
                                              "keep 0.9, Philox-10"}, **gsum)
         # BASELINE configs[3]: MoE block (Mixtral-8x7B-like): 8 experts top-2 SwiGLU FFN 14336
+        log("MoE block")
         mo = rgo.workload_preset("moe")
         mo.philox_rounds = args.rounds
         mblocks, mres, _, mph, _ = run_block_modes(rgo, mo, rank, world, args, modes)
@@ -476,6 +487,7 @@ def bench_block(args, rank, world):
                                             "Philox-10; RNG hidden under 2 + 16 expert GEMMs"}, **msum)
         # batch-chunk pipelining of RNG -> GEMMs -> attention (schedule.hpp:206-239):
         # 4 chunks of one batch item each, live mask = 2 x 64 MiB instead of 256 MiB
+        log("chunked pipeline")
         cmodes = ["serial_fused", "streams", "no_rng"]
         cblocks, cres, _, cph, _ = run_block_modes(rgo, wl, rank, world, args, cmodes, chunks=4)
         for blk in cblocks.values():
@@ -487,10 +499,13 @@ def bench_block(args, rank, world):
                                          "live_mask_mib": 2 * elems // 8 // 4 // 2 ** 20,
                                          "config": "Llama2-7B block, batch split into 4 pipeline stages (mechanism A "
                                                    "per stage, 2-slot mask ring)"}, **csum)
+        log("attention fwd+bwd")
         line["attention_fwd_bwd"] = bench_attention_bwd(rgo, rank, world, peaks)
+        log("SQ sweep")
         line["seq_sweep"] = bench_seq_sweep(rgo, rank, world, (1024, 2048, 4096, 8192, 16384, 32768))
         # reduced-round Philox, stand-alone mask runtime ratios
         # vs the paper's silicon (R5/R7 ~ 0.81, R3/R7 ~ 0.67; PAPER.md 5.2).
+        log("Philox rounds")
         rr = {}
         for R in (3, 5, 7, 10):
             rr[R], _ = bench_mask_kernel(rgo, dict(cfg, rounds=R), rank, 10, 3)
@@ -572,6 +587,7 @@ def main():
     line = bench_block(args, rank, world) if args.workload == "block" else bench_mask_only(args, rank, world)
     if rank == 0:
         if not args.no_cpu_baseline and world == 1:  # the CPU baseline is an N=1 measurement
+            log("CPU baseline (reference, host cores)")
             cb = cpu_reference_block(dict(L, rounds=args.rounds))
             line["cpu_baseline"] = {k: (round(cb[k], 1) if k == "value" else cb[k])
                                     for k in ("value", "unit", "cores", "kind", "sample")}

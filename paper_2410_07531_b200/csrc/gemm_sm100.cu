@@ -5,15 +5,24 @@
 //   C[M, N] = epilogue( alpha * A[M, K] . B[N, K]^T )      (both K-major)
 //
 // * A, B: E4M3 (kind::f8f6f4) or BF16 (kind::f16), fp32 accumulate in TMEM.
-// * Tile 128 x 256 x (128 bytes of K); 4-stage TMA -> smem ring (48 KiB/stage,
-//   SWIZZLE_128B), mbarrier full/empty pipeline.
-// * Warp roles (192 threads): warp 0 = TMA producer, warp 1 = MMA issuer
-//   (one thread issues tcgen05.mma), warps 2-5 = epilogue (TMEM -> registers ->
-//   scale/activation -> bf16 or e4m3 -> global).  Two 256-column TMEM
-//   accumulators (512 columns) so the epilogue of tile i overlaps the MMAs of
-//   tile i+1.
-// * Persistent grid = #SMs, grouped rasterisation (16 M-blocks per group) so
-//   the concurrently running tiles share A rows and B columns in L2.
+// * CTA pairs (cluster of 2, tcgen05 cta_group::2): one 256 x 256 output tile
+//   per pair and step; each CTA stages its 128 rows of A and its 128 rows of
+//   B (half of the tile's N) per 128-byte K slice, the leader CTA issues
+//   tcgen05.mma.cta_group::2 (M = 256) that reads both CTAs' shared memory,
+//   and each CTA's TMEM receives its 128 rows x 256 columns.  Per SM this
+//   halves the B-operand smem/L2 traffic of a 128 x 256 single-CTA tile.
+// * 6-stage TMA -> smem ring per CTA (32 KiB/stage, SWIZZLE_128B); both CTAs'
+//   TMA loads complete on the leader's `full` barrier (cp.async.bulk.tensor
+//   .cta_group::2); MMA completion is multicast to both CTAs' `empty` /
+//   `tfull` barriers (tcgen05.commit.cta_group::2 .multicast::cluster).
+// * Warp roles (192 threads per CTA): warp 0 = TMA producer, warp 1 = MMA
+//   issuer (leader CTA only; one thread issues), warps 2-5 = epilogue (TMEM
+//   -> registers -> scale/activation -> bf16 or e4m3 -> global).  Two
+//   256-column TMEM accumulators so the epilogue of tile i overlaps the MMAs
+//   of tile i+1; the epilogues of both CTAs release an accumulator on the
+//   leader's `tempty` barrier.
+// * Persistent grid = #SMs (74 pairs), grouped rasterisation (16 M-blocks of
+//   256 rows per group) so concurrently running tiles share A and B in L2.
 // * Optional co-resident RNG warps (overlap mechanism B): extra warps that
 //   drain the dropout-mask work queue (csrc/rng_queue.cuh) while the tensor
 //   core runs, using the registers TMEM frees.
@@ -33,12 +42,13 @@
 
 namespace rgo_gk {
 
-constexpr int BM = 128;
-constexpr int BN = 256;
-constexpr int BKB = 128;  // K bytes per stage (64 bf16 / 128 e4m3)
-constexpr int STAGES = 4;
+constexpr int BM = 128;        // rows of A per CTA (the pair's tile has 256)
+constexpr int TILE_M = 2 * BM; // output tile rows per CTA pair
+constexpr int BN = 256;        // output tile columns (each CTA stages BN/2 rows of B)
+constexpr int BKB = 128;       // K bytes per stage (64 bf16 / 128 e4m3)
+constexpr int STAGES = 6;
 constexpr int A_BYTES = BM * BKB;
-constexpr int B_BYTES = BN * BKB;
+constexpr int B_BYTES = (BN / 2) * BKB;
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int GROUP_M = 16;
 constexpr int CORE_THREADS = 192;
@@ -119,10 +129,10 @@ __global__ void __launch_bounds__(CORE_THREADS + 32 * RNG_WARPS, 1)
     uint8_t* smA = smem;
     uint8_t* smB = smem + STAGES * A_BYTES;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-    uint64_t* full = bars;
-    uint64_t* empty = bars + STAGES;
-    uint64_t* tfull = bars + 2 * STAGES;
-    uint64_t* tempty = bars + 2 * STAGES + 2;
+    uint64_t* full = bars;                  // leader: both CTAs' TMA bytes + 2 producer arrivals
+    uint64_t* empty = bars + STAGES;        // each CTA: MMA commit (multicast)
+    uint64_t* tfull = bars + 2 * STAGES;    // each CTA: accumulator ready (multicast commit)
+    uint64_t* tempty = bars + 2 * STAGES + 2;  // leader: 4 epilogue warps x 2 CTAs
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
     volatile int* gemm_done = reinterpret_cast<volatile int*>(tmem_slot + 1);
 
@@ -132,46 +142,53 @@ __global__ void __launch_bounds__(CORE_THREADS + 32 * RNG_WARPS, 1)
     const uint32_t hw_warp = warp_id(), lane = lane_id();
     const bool is_rng_warp = hw_warp < static_cast<uint32_t>(RNG_WARPS);
     const uint32_t warp = is_rng_warp ? CORE_THREADS / 32 + hw_warp : hw_warp - RNG_WARPS;
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < STAGES; ++s) {
-            mbar_init(smem_u32(&full[s]), 1);
+            mbar_init(smem_u32(&full[s]), 2);
             mbar_init(smem_u32(&empty[s]), 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(smem_u32(&tfull[a]), 1);
-            mbar_init(smem_u32(&tempty[a]), 4);
+            mbar_init(smem_u32(&tempty[a]), 8);
         }
         *gemm_done = 0;
         fence_mbar_init();
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
     }
-    if (warp == 1) tmem_alloc<TMEM_COLS>(smem_u32(tmem_slot));
+    if (warp == 1) tmem_alloc2<TMEM_COLS>(smem_u32(tmem_slot));
     tc_fence_before();
-    __syncthreads();
+    cluster_sync_all();  // both CTAs' barriers and TMEM exist before any cross-CTA traffic
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // leader-CTA addresses of the pair-wide barriers
+    const uint32_t full0_leader = mapa_shared(smem_u32(&full[0]), 0);
+    const uint32_t tempty0_leader = mapa_shared(smem_u32(&tempty[0]), 0);
 
+    const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
     const int num_tiles = p.tiles_m * p.tiles_n;
     const int kblocks = (p.K * (FP8 ? 1 : 2)) / BKB;
     const int bk_elems = FP8 ? BKB : BKB / 2;
-    constexpr uint32_t IDESC = FP8 ? idesc_make(0, 0, BM, BN, 0, 0) : idesc_make(1, 1, BM, BN, 0, 0);
+    constexpr uint32_t IDESC = FP8 ? idesc_make(0, 0, TILE_M, BN, 0, 0) : idesc_make(1, 1, TILE_M, BN, 0, 0);
 
     if (warp == 0) {  // ---------------- TMA producer (whole warp loops, one lane issues)
         int stage = 0;
         uint32_t phase = 0;
-        const uint32_t sa = smem_u32(smA), sb = smem_u32(smB), fb0 = smem_u32(&full[0]), eb0 = smem_u32(&empty[0]);
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const uint32_t sa = smem_u32(smA), sb = smem_u32(smB), eb0 = smem_u32(&empty[0]);
+        for (int tile = pair; tile < num_tiles; tile += n_pairs) {
             int mb, nb;
             tile_coords(tile, p.tiles_m, p.tiles_n, mb, nb);
-            const int row_a = mb * BM, row_b = nb * BN;
+            const int row_a = mb * TILE_M + rank * BM, row_b = nb * BN + rank * (BN / 2);
             for (int kb = 0; kb < kblocks; ++kb) {
                 mbar_wait(eb0 + 8 * stage, phase ^ 1);
                 if (elect_one()) {
-                    const uint32_t fb = fb0 + 8 * stage;
-                    mbar_arrive_expect_tx(fb, STAGE_BYTES);
-                    tma_load_2d(sa + stage * A_BYTES, &tmA, fb, kb * bk_elems, row_a);
-                    tma_load_2d(sb + stage * B_BYTES, &tmB, fb, kb * bk_elems, row_b);
+                    const uint32_t fb = full0_leader + 8 * stage;
+                    if (leader) mbar_arrive_expect_tx(fb, 2 * STAGE_BYTES);
+                    tma_load_2d_pair(sa + stage * A_BYTES, &tmA, fb, kb * bk_elems, row_a);
+                    tma_load_2d_pair(sb + stage * B_BYTES, &tmB, fb, kb * bk_elems, row_b);
+                    if (!leader) mbar_arrive_cluster(fb);
                 }
                 __syncwarp();
                 if (++stage == STAGES) {
@@ -180,52 +197,54 @@ __global__ void __launch_bounds__(CORE_THREADS + 32 * RNG_WARPS, 1)
                 }
             }
         }
-    } else if (warp == 1) {  // ---------------- MMA issuer (whole warp loops, one lane issues)
-        int stage = 0;
-        uint32_t phase = 0, acc = 0, acc_phase = 0;
-        // descriptors of stage 0; stage s adds s*STAGE/16 to the start-address field
-        const uint64_t ad0 = desc_kmajor_sw128(smem_u32(smA)), bd0 = desc_kmajor_sw128(smem_u32(smB));
-        const uint32_t fb0 = smem_u32(&full[0]), eb0 = smem_u32(&empty[0]);
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-            mbar_wait(smem_u32(&tempty[acc]), acc_phase ^ 1);
-            tc_fence_after();
-            const uint32_t d = tmem_base + acc * BN;
-            for (int kb = 0; kb < kblocks; ++kb) {
-                mbar_wait(fb0 + 8 * stage, phase);
+    } else if (warp == 1) {  // ---------------- MMA issuer (leader CTA; whole warp loops, one lane issues)
+        if (leader) {
+            int stage = 0;
+            uint32_t phase = 0, acc = 0, acc_phase = 0;
+            // descriptors of stage 0; stage s adds s*STAGE/16 to the start-address field
+            const uint64_t ad0 = desc_kmajor_sw128(smem_u32(smA)), bd0 = desc_kmajor_sw128(smem_u32(smB));
+            const uint32_t fb0 = smem_u32(&full[0]), eb0 = smem_u32(&empty[0]);
+            for (int tile = pair; tile < num_tiles; tile += n_pairs) {
+                mbar_wait(smem_u32(&tempty[acc]), acc_phase ^ 1);
                 tc_fence_after();
-                if (elect_one()) {
-                    const uint64_t ad = ad0 + static_cast<uint64_t>(stage * (A_BYTES >> 4));
-                    const uint64_t bd = bd0 + static_cast<uint64_t>(stage * (B_BYTES >> 4));
+                const uint32_t d = tmem_base + acc * BN;
+                for (int kb = 0; kb < kblocks; ++kb) {
+                    mbar_wait(fb0 + 8 * stage, phase);
+                    tc_fence_after();
+                    if (elect_one()) {
+                        const uint64_t ad = ad0 + static_cast<uint64_t>(stage * (A_BYTES >> 4));
+                        const uint64_t bd = bd0 + static_cast<uint64_t>(stage * (B_BYTES >> 4));
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {  // 4 x 32 bytes of K per stage
-                        const uint32_t acc_flag = (kb | k) != 0;
-                        if constexpr (FP8)
-                            mma_f8_ss(d, ad + 2 * k, bd + 2 * k, IDESC, acc_flag);
-                        else
-                            mma_f16_ss(d, ad + 2 * k, bd + 2 * k, IDESC, acc_flag);
+                        for (int k = 0; k < 4; ++k) {  // 4 x 32 bytes of K per stage
+                            const uint32_t acc_flag = (kb | k) != 0;
+                            if constexpr (FP8)
+                                mma2_f8_ss(d, ad + 2 * k, bd + 2 * k, IDESC, acc_flag);
+                            else
+                                mma2_f16_ss(d, ad + 2 * k, bd + 2 * k, IDESC, acc_flag);
+                        }
+                        tc_commit2_mc(eb0 + 8 * stage);
+                        if (kb == kblocks - 1) tc_commit2_mc(smem_u32(&tfull[acc]));
                     }
-                    tc_commit(eb0 + 8 * stage);
-                    if (kb == kblocks - 1) tc_commit(smem_u32(&tfull[acc]));
+                    __syncwarp();
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
                 }
-                __syncwarp();
-                if (++stage == STAGES) {
-                    stage = 0;
-                    phase ^= 1;
-                }
+                acc ^= 1;
+                if (acc == 0) acc_phase ^= 1;
             }
-            acc ^= 1;
-            if (acc == 0) acc_phase ^= 1;
         }
-    } else if (warp < CORE_THREADS / 32) {  // ---------------- epilogue warps 2..5
+    } else if (warp < CORE_THREADS / 32) {  // ---------------- epilogue warps 2..5 (both CTAs)
         const uint32_t q = hw_warp & 3;  // TMEM lane quarter = physical warp id % 4
-        const int row_in_tile = q * 32 + lane;
+        const int row_in_tile = static_cast<int>(rank) * BM + q * 32 + lane;
         uint32_t acc = 0, acc_phase = 0;
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        for (int tile = pair; tile < num_tiles; tile += n_pairs) {
             int mb, nb;
             tile_coords(tile, p.tiles_m, p.tiles_n, mb, nb);
             mbar_wait(smem_u32(&tfull[acc]), acc_phase);
             tc_fence_after();
-            const int row = mb * BM + row_in_tile;
+            const int row = mb * TILE_M + row_in_tile;
             const uint32_t tbase = tmem_base + ((q * 32) << 16) + acc * BN;
             if constexpr (EPI == EPI_SWIGLU) {
 #pragma unroll 1
@@ -262,7 +281,7 @@ __global__ void __launch_bounds__(CORE_THREADS + 32 * RNG_WARPS, 1)
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(smem_u32(&tempty[acc]));
+            if (lane == 0) mbar_arrive_cluster(tempty0_leader + 8 * acc);
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
         }
@@ -278,8 +297,9 @@ __global__ void __launch_bounds__(CORE_THREADS + 32 * RNG_WARPS, 1)
             if (lane == 0) atomicAdd(const_cast<int*>(gemm_done), 1);
         }
     }
-    __syncthreads();
-    if (warp == 1) tmem_dealloc<TMEM_COLS>(tmem_base);
+    tc_fence_before();
+    cluster_sync_all();  // the peer's last MMAs / remote arrivals are done before TMEM goes
+    if (warp == 1) tmem_dealloc2<TMEM_COLS>(tmem_base);
 }
 
 template <bool FP8, int EPI, int OUT, int RNG_WARPS>
@@ -292,8 +312,19 @@ static cudaError_t launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const 
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    k<<<grid, CORE_THREADS + 32 * RNG_WARPS, SMEM_BYTES, s>>>(ta, tb, p);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3(CORE_THREADS + 32 * RNG_WARPS);
+    cfg.dynamicSmemBytes = SMEM_BYTES;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k, ta, tb, p);
 }
 
 }  // namespace rgo_gk
@@ -318,7 +349,7 @@ cudaError_t launch_gemm(const GemmJob& j, cudaStream_t s) {
     {
         const uint64_t dims[2] = {static_cast<uint64_t>(j.K), static_cast<uint64_t>(j.N)};
         const uint64_t strides[1] = {static_cast<uint64_t>(j.ldb) * esz};
-        const uint32_t box[2] = {static_cast<uint32_t>(BKB / esz), BN};
+        const uint32_t box[2] = {static_cast<uint32_t>(BKB / esz), BN / 2};
         if (!make_tmap(&tb, j.B, dt, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B))
             return cudaErrorInvalidValue;
     }
@@ -326,7 +357,7 @@ cudaError_t launch_gemm(const GemmJob& j, cudaStream_t s) {
     p.M = j.M;
     p.N = j.N;
     p.K = j.K;
-    p.tiles_m = (j.M + BM - 1) / BM;
+    p.tiles_m = (j.M + TILE_M - 1) / TILE_M;
     p.tiles_n = (j.N + BN - 1) / BN;
     p.C = j.C;
     p.ldc = j.ldc;
@@ -336,7 +367,9 @@ cudaError_t launch_gemm(const GemmJob& j, cudaStream_t s) {
     if (j.rng) p.rng = *j.rng;
     const int tiles = p.tiles_m * p.tiles_n;
     int grid = j.grid > 0 ? j.grid : num_sms();
-    if (grid > tiles) grid = tiles;
+    if (grid > 2 * tiles) grid = 2 * tiles;
+    grid &= ~1;  // whole CTA pairs
+    if (grid < 2) grid = 2;
     const bool rng = j.rng != nullptr;
     const int rw = j.rng_warps ? j.rng_warps : RNG_WARPS_IN_GEMM;
 #define RGO_G(F, E, O)                                                                  \

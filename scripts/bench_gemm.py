@@ -33,8 +33,18 @@ for dt in (torch.float8_e4m3fn, torch.bfloat16):
                 torch.matmul(a, b.T)
             e1.record(); torch.cuda.synchronize()
             cub = e0.elapsed_time(e1) / n
-        else:
-            cub = None
+        else:  # cuBLASLt FP8 (torch._scaled_mm, per-tensor scales, bf16 out)
+            one = torch.ones((), device="cuda")
+            try:
+                torch._scaled_mm(a, b.T, scale_a=one, scale_b=one, out_dtype=torch.bfloat16)
+                torch.cuda.synchronize()
+                e0.record()
+                for _ in range(n):
+                    torch._scaled_mm(a, b.T, scale_a=one, scale_b=one, out_dtype=torch.bfloat16)
+                e1.record(); torch.cuda.synchronize()
+                cub = e0.elapsed_time(e1) / n
+            except Exception as ex:  # noqa: BLE001
+                cub = f"unavailable: {ex}"[:80]
         res.append({"gemm": sh.name, "dtype": str(dt), "m": sh.m, "n": sh.n, "k": sh.k, "ms": round(ms, 4),
                     "tflops": round(tf, 1), "cublas_ms": cub})
         print(json.dumps(res[-1]), flush=True)
