@@ -1172,6 +1172,21 @@ static bool tmap4(CUtensorMap* m, const AttnTensor& t, int B, int H, int S, int 
     return make_tmap(m, t.ptr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
+// Experiment switches, read once per process (not per call): RGO_BWD_DEBUG=1
+// skips the dQ reductions (timing only -- dQ is then wrong), RGO_BWD_V1=1
+// runs the 128-query-tile kernel for head_dim 128 as well.
+static int bwd_debug_flags() {
+    static const int v = [] {
+        const char* d = getenv("RGO_BWD_DEBUG");
+        return d ? atoi(d) : 0;
+    }();
+    return v;
+}
+static bool bwd_force_v1() {
+    static const bool v = getenv("RGO_BWD_V1") != nullptr;
+    return v;
+}
+
 static void fill_params(rgo_attn_bwd::Params& p, const AttnBwdJob& j, int n_qt, float* rowbuf, float* dq_acc) {
     using namespace rgo_attn_bwd;
     p.B = j.B; p.H = j.H; p.S = j.S;
@@ -1192,7 +1207,7 @@ static void fill_params(rgo_attn_bwd::Params& p, const AttnBwdJob& j, int n_qt, 
     p.dq_acc = dq_acc;
     p.dK = j.dk.ptr; p.k_sb = j.dk.sb; p.k_sh = j.dk.sh; p.k_ss = j.dk.ss;
     p.dV = j.dv.ptr; p.v_sb = j.dv.sb; p.v_sh = j.dv.sh; p.v_ss = j.dv.ss;
-    if (const char* dbg = getenv("RGO_BWD_DEBUG")) p.debug = atoi(dbg);
+    p.debug = bwd_debug_flags();
 }
 
 // head_dim 128: the 64-query-tile kernel (double-buffered dQ^T in TMEM).
@@ -1234,7 +1249,7 @@ static cudaError_t launch_attn_bwd2(const AttnBwdJob& j, cudaStream_t s) {
 
 cudaError_t launch_attn_bwd(const AttnBwdJob& j, cudaStream_t s) {
     using namespace rgo_attn_bwd;
-    if (j.HD == 128 && !getenv("RGO_BWD_V1")) return launch_attn_bwd2(j, s);
+    if (j.HD == 128 && !bwd_force_v1()) return launch_attn_bwd2(j, s);
     CUtensorMap tq, tk, tv, tdo;
     if (!tmap4(&tq, j.q, j.B, j.H, j.S, j.HD) || !tmap4(&tk, j.k, j.B, j.H, j.S, j.HD) ||
         !tmap4(&tv, j.v, j.B, j.H, j.S, j.HD) || !tmap4(&tdo, j.dout, j.B, j.H, j.S, j.HD))
@@ -1273,7 +1288,7 @@ cudaError_t launch_attn_bwd(const AttnBwdJob& j, cudaStream_t s) {
     p.dV = j.dv.ptr; p.v_sb = j.dv.sb; p.v_sh = j.dv.sh; p.v_ss = j.dv.ss;
     int mode = j.mode;
     if (mode == rgo_attn::MASK_PHILOX && j.threshold >= (uint64_t{1} << 32)) mode = rgo_attn::MASK_NONE;
-    if (const char* dbg = getenv("RGO_BWD_DEBUG")) p.debug = atoi(dbg);
+    p.debug = bwd_debug_flags();
     cudaError_t e = cudaErrorInvalidValue;
 #define RGO_B(HDV, MODEV, RV) \
     if (j.HD == HDV && mode == MODEV) { e = launch_main<HDV, MODEV, RV>(tq, tk, tv, tdo, p, s); goto launched; }
