@@ -198,14 +198,14 @@ static cudaError_t enqueue_step(Block& b, int* launches) {
         if ((e = cudaEventRecord(b.ev_fork, s)) != cudaSuccess) return e;
         if ((e = cudaStreamWaitEvent(b.s_rng, b.ev_fork, 0)) != cudaSuccess) return e;
         MaskJob mj{x.mask, elems, c.seed, c.base_offset, c.threshold, c.rounds};
-        // Default shape: one 128-thread CTA per SM (one RNG warp per SMSP):
-        // it always fits beside a resident GEMM CTA, and a sweep over 1-3
-        // CTAs of 128/256 threads per SM (scripts/sweep_overlap.py) finds the
-        // fewest RNG warps fastest -- more of them slow the GEMM more than
-        // they speed up the mask.
+        // Default shape: one 256-thread CTA per SM (two RNG warps per SMSP):
+        // it always fits beside a resident GEMM CTA.  Interleaved sweeps
+        // (scripts/sweep_overlap.py) over 64-512 threads and 0.5-2 CTAs per
+        // SM: with the 2-SM GEMMs this shape finishes the mask inside the GEMM
+        // window without slowing the GEMMs more than it gains.
         LaunchShape ls;
         ls.grid = c.rng_grid ? c.rng_grid : static_cast<unsigned>(num_sms());
-        ls.block = c.rng_block ? c.rng_block : 128;
+        ls.block = c.rng_block ? c.rng_block : 256;
         ls.dyn_smem = c.rng_smem;
         if ((e = launch_mask(mj, ls, b.s_rng)) != cudaSuccess) return e;
         ++n;
@@ -345,7 +345,7 @@ static cudaError_t enqueue_step_chunked(Block& b, int* launches) {
             MaskJob mj{bits, chunk_elems, c.seed, base, c.threshold, c.rounds};
             LaunchShape ls;
             ls.grid = c.rng_grid ? c.rng_grid : static_cast<unsigned>(num_sms());
-            ls.block = c.rng_block ? c.rng_block : 128;
+            ls.block = c.rng_block ? c.rng_block : 256;
             ls.dyn_smem = c.rng_smem;
             if ((e = launch_mask(mj, ls, b.s_rng)) != cudaSuccess) return e;
             ++n;

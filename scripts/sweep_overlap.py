@@ -29,7 +29,7 @@ def run(mode, launch=(0, 0, 0), steps=10):
 
 configs = [("no_rng", (0, 0, 0)), ("serial_fused", (0, 0, 0)), ("in_gemm", (0, 6, 0)), ("in_gemm", (0, 8, 0)),
            ("streams", (148, 128, 0)), ("streams", (148, 256, 0)), ("streams", (148, 64, 0)),
-           ("streams", (74, 128, 0))]
+           ("streams", (74, 128, 0)), ("streams", (148, 512 // 2, 0)), ("streams", (296, 128, 0))]
 # three passes in alternating order: the 1 kW power state drifts during a run
 for rep in range(3):
     for mode, launch in (configs if rep % 2 == 0 else configs[::-1]):
