@@ -61,8 +61,9 @@ class ClockSampler:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
                                       "--format=csv,noheader,nounits"], capture_output=True, text=True,
                                      timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                fields = [x.strip() for x in out.split(",")] if out else []
+                if len(fields) == 7:  # skip error text (e.g. an index with no device)
+                    self.samples.append(fields)
             except Exception:
                 pass
             self._stop.wait(0.02)
@@ -98,8 +99,15 @@ def dist_setup():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # one process per GPU; BENCH_DIST_BACKEND=gloo with more ranks than GPUs
+        # lets the multi-rank code paths be exercised on a single device
+        dev = local % max(1, torch.cuda.device_count())
+        torch.cuda.set_device(dev)
+        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
     return rank, world, local
@@ -349,7 +357,7 @@ def bench_block(args, rank, world):
     modes = ["serial_fused", "streams", "in_gemm", "no_rng"]
     peaks, src = load_peaks()
     log("Llama2-7B block modes")
-    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+    with ClockSampler(torch.cuda.current_device()) as clk:
         blocks, res, samples, phases, launches = run_block_modes(rgo, wl, rank, world, args, modes)
     log("mask kernel")
     att_ms = phases["no_rng"][1]  # the mask-reading attention kernel alone, in situ
@@ -530,7 +538,8 @@ def profiled_traffic(kernel):
 def bench_mask_only(args, rank, world):
     import paper_2410_07531_b200 as rgo
     cfg = dict(L, rounds=args.rounds)
-    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+    import torch
+    with ClockSampler(torch.cuda.current_device()) as clk:
         ms, elems = bench_mask_kernel(rgo, cfg, rank, args.steps, args.warmup)
     ms = max_over_ranks(ms, world)
     peaks, src = load_peaks()
