@@ -49,6 +49,7 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
 
 #include "attn.h"
 #include "philox.cuh"
@@ -89,6 +90,7 @@ struct Params {
     long long k_sb, k_sh, k_ss;  // dK strides (elements)
     long long v_sb, v_sh, v_ss;  // dV strides
     int debug;                   // experiment switches (RGO_BWD_DEBUG), 0 in production
+    int mask_tma;                // v2, MASK_BITS: the keep-bit tile arrives by TMA with Q (SQ % 128 == 0)
 };
 
 // Blocked dQ accumulator: per (slice, query tile) HD/32 column chunks of 8
@@ -700,7 +702,8 @@ struct Smem2 {
     static constexpr int STG_OFF = DS_OFF + 128 * 128;      // 2 x dQ^T tile (128 x 64 fp32)
     static constexpr int STG_BYTES = 128 * BQ2 * 4;
     static constexpr int ROW_OFF = STG_OFF + 2 * STG_BYTES; // per stage: 64 -lse2, 64 D
-    static constexpr int BAR_OFF = ROW_OFF + 2 * 512;
+    static constexpr int MSK_OFF = ROW_OFF + 2 * 512;        // per stage: 64 query rows x 16 B of keep bits
+    static constexpr int BAR_OFF = MSK_OFF + 2 * 1024;
     static constexpr int BYTES = BAR_OFF + 256;
     static constexpr int ALLOC = BYTES + 1023;
 };
@@ -785,6 +788,7 @@ __global__ void __launch_bounds__(THREADS, 1) bwd_main2_kernel(const __grid_cons
                                                                const __grid_constant__ CUtensorMap tmK,
                                                                const __grid_constant__ CUtensorMap tmV,
                                                                const __grid_constant__ CUtensorMap tmdO,
+                                                               const __grid_constant__ CUtensorMap tmM,
                                                                const Params p) {
     using SM = Smem2;
     constexpr int HD = 128;
@@ -866,10 +870,13 @@ __global__ void __launch_bounds__(THREADS, 1) bwd_main2_kernel(const __grid_cons
             mbar_wait(smem_u32(&q_empty[st]), ph ^ 1);
             if (elect_one()) {
                 const uint32_t qb = smem_u32(&q_full[st]);
-                mbar_arrive_expect_tx(qb, SM::QTILE + 512);
+                mbar_arrive_expect_tx(qb, SM::QTILE + 512 + (p.mask_tma ? 1024 : 0));
                 for (int c = 0; c < 2; ++c)
                     tma_load_4d(smem_u32(sQ + st * SM::QTILE + c * SM::QCHUNK), &tmQ, qb, c * 64, qt * BQ2, hh, bb);
                 bulk_load(smem_u32(smem + SM::ROW_OFF + st * 512), rows + qt * (2 * BQ2), 512, qb);
+                if (MODE == MASK_BITS && p.mask_tma)  // keep bits of (64 query rows) x (this CTA's 128 keys)
+                    tma_load_2d(smem_u32(smem + SM::MSK_OFF + st * 1024), &tmM, qb, kv0 / 8,
+                                static_cast<int>(slice) * p.S + qt * BQ2);
             }
             __syncwarp();
             mbar_wait(smem_u32(&do_empty[st]), ph ^ 1);
@@ -977,13 +984,19 @@ __global__ void __launch_bounds__(THREADS, 1) bwd_main2_kernel(const __grid_cons
             const int st = i & 1;
             const uint32_t ph = (i >> 1) & 1;
             const int qrow = qtile(i) * BQ2 + 32 * h + static_cast<int>(lane);
-            uint32_t w = 0;
-            if (qrow < p.S) w = row_word<MODE, R>(p, (slice * p.S + qrow) * static_cast<uint64_t>(p.S) + kcol, kvalid);
-            uint32_t kw = transpose32(w, lane);  // bit e: keep(query tile*64 + 32h + e, key kv0 + r)
-            if (!key_valid) kw = 0;
             const float* nlse = sRows + st * 128 + 32 * h;
             const float* Dv = nlse + BQ2;
-            mbar_wait(smem_u32(&q_full[st]), ph);  // row terms of tile i landed
+            uint32_t w = 0;
+            if (MODE == MASK_BITS && p.mask_tma) {  // this lane's query row, this warp's 32 keys, from smem
+                mbar_wait(smem_u32(&q_full[st]), ph);  // row terms and mask tile of tile i landed
+                w = reinterpret_cast<const uint32_t*>(smem + SM::MSK_OFF + st * 1024)[(32 * h + lane) * 4 + qw];
+            } else {
+                if (qrow < p.S)
+                    w = row_word<MODE, R>(p, (slice * p.S + qrow) * static_cast<uint64_t>(p.S) + kcol, kvalid);
+                mbar_wait(smem_u32(&q_full[st]), ph);  // row terms of tile i landed
+            }
+            uint32_t kw = transpose32(w, lane);  // bit e: keep(query tile*64 + 32h + e, key kv0 + r)
+            if (!key_valid) kw = 0;
             mbar_wait(smem_u32(s_full), i & 1);
             tc_fence_after();
             uint32_t pb[16];
@@ -1125,7 +1138,7 @@ __global__ void __launch_bounds__(THREADS, 1) bwd_main2_kernel(const __grid_cons
 
 template <int MODE, int R>
 static cudaError_t launch_main2(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
-                                const CUtensorMap& dO, const Params& p, cudaStream_t s) {
+                                const CUtensorMap& dO, const CUtensorMap& m, const Params& p, cudaStream_t s) {
     auto kern = bwd_main2_kernel<MODE, R>;
     static bool attr = false;
     if (!attr) {
@@ -1134,7 +1147,7 @@ static cudaError_t launch_main2(const CUtensorMap& q, const CUtensorMap& k, cons
         attr = true;
     }
     const unsigned grid = static_cast<unsigned>(p.B) * p.H * p.n_kt;
-    kern<<<grid, THREADS, Smem2::ALLOC, s>>>(q, k, v, dO, p);
+    kern<<<grid, THREADS, Smem2::ALLOC, s>>>(q, k, v, dO, m, p);
     return cudaGetLastError();
 }
 
@@ -1235,11 +1248,22 @@ static cudaError_t launch_attn_bwd2(const AttnBwdJob& j, cudaStream_t s) {
     fill_params(p, j, n_qt, rowbuf, dq_acc);
     int mode = j.mode;
     if (mode == rgo_attn::MASK_PHILOX && j.threshold >= (uint64_t{1} << 32)) mode = rgo_attn::MASK_NONE;
-    if (mode == rgo_attn::MASK_NONE) e = launch_main2<rgo_attn::MASK_NONE, 0>(tq, tk, tv, tdo, p, s);
-    else if (mode == rgo_attn::MASK_BITS) e = launch_main2<rgo_attn::MASK_BITS, 0>(tq, tk, tv, tdo, p, s);
-    else if (j.rounds == 10) e = launch_main2<rgo_attn::MASK_PHILOX, 10>(tq, tk, tv, tdo, p, s);
-    else if (j.rounds == 7) e = launch_main2<rgo_attn::MASK_PHILOX, 7>(tq, tk, tv, tdo, p, s);
-    else e = launch_main2<rgo_attn::MASK_PHILOX, 0>(tq, tk, tv, tdo, p, s);
+    // keep-bit tiles by TMA: the mask as a 2-D byte array [B*H*S rows][S/8 bytes],
+    // box = 16 bytes (128 keys) x 64 query rows
+    CUtensorMap tm;
+    std::memset(&tm, 0, sizeof(tm));
+    if (mode == rgo_attn::MASK_BITS && j.S % 128 == 0 && (reinterpret_cast<uintptr_t>(j.bits) & 15) == 0) {
+        const uint64_t dims[2] = {static_cast<uint64_t>(j.S) / 8, static_cast<uint64_t>(j.B) * j.H * j.S};
+        const uint64_t strides[1] = {static_cast<uint64_t>(j.S) / 8};
+        const uint32_t box[2] = {16, static_cast<uint32_t>(BQ2)};
+        p.mask_tma = make_tmap(&tm, j.bits, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, dims, strides, box,
+                               CU_TENSOR_MAP_SWIZZLE_NONE) ? 1 : 0;
+    }
+    if (mode == rgo_attn::MASK_NONE) e = launch_main2<rgo_attn::MASK_NONE, 0>(tq, tk, tv, tdo, tm, p, s);
+    else if (mode == rgo_attn::MASK_BITS) e = launch_main2<rgo_attn::MASK_BITS, 0>(tq, tk, tv, tdo, tm, p, s);
+    else if (j.rounds == 10) e = launch_main2<rgo_attn::MASK_PHILOX, 10>(tq, tk, tv, tdo, tm, p, s);
+    else if (j.rounds == 7) e = launch_main2<rgo_attn::MASK_PHILOX, 7>(tq, tk, tv, tdo, tm, p, s);
+    else e = launch_main2<rgo_attn::MASK_PHILOX, 0>(tq, tk, tv, tdo, tm, p, s);
     if (e != cudaSuccess) return e;
     const uint64_t n = static_cast<uint64_t>(j.B) * j.H * n_qt * 256;
     bwd_dq2_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
