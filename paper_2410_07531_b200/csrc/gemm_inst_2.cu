@@ -1,0 +1,7 @@
+// gemm_inst_2.cu -- explicit instantiations of the CTA-pair GEMM (gemm_sm100.cuh).
+#include "gemm_sm100.cuh"
+
+namespace rgo_gk {
+RGO_GEMM_VARIANT(true, EPI_GELU, OUT_E4M3)
+RGO_GEMM_VARIANT(false, EPI_NONE, OUT_BF16)
+}  // namespace rgo_gk

@@ -1,0 +1,7 @@
+// gemm_inst_3.cu -- explicit instantiations of the CTA-pair GEMM (gemm_sm100.cuh).
+#include "gemm_sm100.cuh"
+
+namespace rgo_gk {
+RGO_GEMM_VARIANT(false, EPI_SWIGLU, OUT_BF16)
+RGO_GEMM_VARIANT(false, EPI_GELU, OUT_BF16)
+}  // namespace rgo_gk
