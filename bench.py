@@ -315,6 +315,26 @@ def bench_attention_bwd(rgo, rank, world, peaks):
     return out
 
 
+def bench_flash_attn(world):
+    """The installed flash-attn (FA2, Philox fused in the kernel) with dropout 0.1
+    at the Llama2-7B attention shape: the library form of the conventional
+    fused-dropout baseline (PAPER's comparison), timed beside ours."""
+    import torch
+    try:
+        import flash_attn
+        from flash_attn import flash_attn_func
+    except Exception as e:  # noqa: BLE001
+        return {"unavailable": str(e)[:120]}
+    B, H, S, D = L["batch"], L["heads"], L["seq"], L["head_dim"]
+    q, k, v = ((torch.rand(B, S, H, D, device="cuda") * 2 - 1).bfloat16().requires_grad_(True) for _ in range(3))
+    do = (torch.rand(B, S, H, D, device="cuda") * 2 - 1).bfloat16()
+    fwd = event_ms(lambda: flash_attn_func(q, k, v, dropout_p=1.0 - L["keep_prob"]), 5, world, warm=2)
+    o = flash_attn_func(q, k, v, dropout_p=1.0 - L["keep_prob"])
+    bwd = event_ms(lambda: torch.autograd.grad(o, (q, k, v), do, retain_graph=True), 5, world, warm=2)
+    return {"version": flash_attn.__version__, "fwd_ms": round(fwd, 4), "bwd_ms": round(bwd, 4),
+            "config": "flash_attn_func(dropout_p=0.1), B4 S4096 H32 D128 bf16 (sm_100 runs its sm80 kernels)"}
+
+
 def bench_seq_sweep(rgo, rank, world, lens):
     """BASELINE configs[4]: SQ sweep at the Llama2 head config (B1 nH32 dH128),
     batch x head sharded over the ranks (rank r owns heads [r*32/n, (r+1)*32/n)
@@ -509,6 +529,15 @@ def bench_block(args, rank, world):
                                                    "per stage, 2-slot mask ring)"}, **csum)
         log("attention fwd+bwd")
         line["attention_fwd_bwd"] = bench_attention_bwd(rgo, rank, world, peaks)
+        log("flash-attn library baseline")
+        line["flash_attn_dropout_baseline"] = bench_flash_attn(world)
+        fa = line["flash_attn_dropout_baseline"]
+        if "fwd_ms" in fa:
+            # the block step with the library's fused-dropout attention in place of
+            # ours: this run's GEMM window + flash-attn's forward (composed, not one graph)
+            comp = summ["phases_ms"]["serial_fused"]["gemm_window"] + fa["fwd_ms"]
+            line["speedup_vs_flash_attn_block"] = {"composed_ms": round(comp, 4),
+                                                   "speedup": round(comp / value, 4)}
         log("SQ sweep")
         line["seq_sweep"] = bench_seq_sweep(rgo, rank, world, (1024, 2048, 4096, 8192, 16384, 32768))
         # reduced-round Philox, stand-alone mask runtime ratios
