@@ -11,6 +11,7 @@
 #include "rgo/mask.hpp"
 #include "rgo/philox.hpp"
 #include "rgo/ref_attention.hpp"
+#include "rgo/schedule.hpp"
 #include "rgo/workload.hpp"
 
 extern "C" {
@@ -131,6 +132,32 @@ void ref_philox_test_vectors(uint64_t seed, int count, int rounds_fixed, uint32_
         std::memcpy(ctrs + 4 * t, c, 16);
         rounds[t] = r;
         words[4 * t] = b.w0; words[4 * t + 1] = b.w1; words[4 * t + 2] = b.w2; words[4 * t + 3] = b.w3;
+    }
+}
+
+// The reference's timeline composition (schedule.hpp:111-136) on given kernel
+// times: in = {gemm_total, attn, rng, fused} seconds, cal = {f_gemm_under_rng,
+// f_rng_under_gemm, f_drop, f_carve}; out = {t_baseline, t_overlap, speedup,
+// t_rng_exposed}.  Used to check the B200 calibration script's restatement.
+int ref_compose_schedule(const double in[4], const double cal[4], double out[4]) {
+    try {
+        rgo::KernelEstimate attn, rng, fused;
+        attn.runtime_s = in[1];
+        rng.runtime_s = in[2];
+        fused.runtime_s = in[3];
+        rgo::CalibrationFactors c;
+        c.f_gemm_under_rng = cal[0];
+        c.f_rng_under_gemm = cal[1];
+        c.f_drop = cal[2];
+        c.f_carve = cal[3];
+        const rgo::ScheduleEstimate e = rgo::compose_schedule(in[0], attn, rng, fused, c);
+        out[0] = e.t_baseline_s;
+        out[1] = e.t_overlap_s;
+        out[2] = e.speedup;
+        out[3] = e.t_rng_exposed_s;
+        return 0;
+    } catch (const std::invalid_argument&) {
+        return -1;
     }
 }
 
