@@ -451,6 +451,8 @@ def bench_block(args, rank, world):
                    "overlap_mechanism": best,
                    "l2": "no flush: every step streams > 1 GB (mask 256 MiB, QKV 384 MiB) through a 126 MB L2"},
         "speedup_vs_fused": summ["speedup_vs_fused"],
+        # the paper's block speedups (GH100, FP8); ours are measured on B200
+        "paper_speedup_gh100": {"llama2": 1.14, "moe": 1.13, "gpt3": 1.06, "source": "PAPER.md:57,197"},
         "modes_ms": summ["modes_ms"],
         "modes_ms_samples": {m: [round(x, 4) for x in v] for m, v in samples.items()},
         "phases_ms": summ["phases_ms"],
