@@ -310,6 +310,9 @@ int rgo_block_create(const rgo_block_desc* d, const rgo_block_buffers* b, int32_
 int rgo_block_step(rgo_block* blk, rgo_stream_t stream, int32_t* launches);
 /* Device time (ms) of the last completed step: [0] GEMM window, [1] attention. */
 int rgo_block_last_timings(rgo_block* blk, float* ms2);
+/* Finer split: [0] GEMM window, [1] RNG tail drain / join before the attention,
+ * [2] the attention kernel. */
+int rgo_block_last_timings3(rgo_block* blk, float* ms3);
 int rgo_block_destroy(rgo_block* blk);
 
 #ifdef __cplusplus

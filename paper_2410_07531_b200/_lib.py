@@ -132,6 +132,7 @@ SIGNATURES = {
     "rgo_block_create": (C.c_int, [C.POINTER(block_desc), C.POINTER(block_buffers), C.c_int32, C.c_void_p]),
     "rgo_block_step": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "rgo_block_last_timings": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "rgo_block_last_timings3": (C.c_int, [C.c_void_p, C.c_void_p]),
     "rgo_block_destroy": (C.c_int, [C.c_void_p]),
     "rgo_philox_blocks_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64]),
     "rgo_random_attention_input_host": (

@@ -59,6 +59,17 @@ class Block:
         self.chunks = max(1, chunks)
         live = elems if self.chunks == 1 else 2 * (elems // self.chunks)
         self.mask = torch.zeros(live // 8, dtype=torch.uint8, device=dev)
+        if mode == "no_rng":
+            # NO_RNG never writes the mask; give its attention the real keep pattern
+            # (an all-zero mask would feed the tensor cores zeros -- less power, higher
+            # clock -- and make this measurement floor optimistic)
+            from .mask import MaskLayout, generate_mask_device
+            n_slices = B * H if self.chunks == 1 else (B // self.chunks) * H
+            lay = MaskLayout(1, n_slices, S, seed, base_offset)
+            for c in range(1 if self.chunks == 1 else 2):
+                part = self.mask[c * (live // 8 // (1 if self.chunks == 1 else 2)):]
+                generate_mask_device(lay, KeepThreshold(cfg.keep_prob), cfg.philox_rounds, out=part[: lay.elem_count() // 8])
+            torch.cuda.synchronize()
         self.counter = torch.zeros(1, dtype=torch.int64, device=dev)
         self.lse = None
         ku = 3.0  # E[(U(-1,1))^2] = 1/3 -> alpha = 3/sqrt(K) gives unit-variance outputs
@@ -100,6 +111,12 @@ class Block:
         arr = (C.c_float * 2)()
         _lib.check(_lib.lib().rgo_block_last_timings(self.handle, arr))
         return float(arr[0]), float(arr[1])
+
+    def last_timings3(self):
+        """(GEMM window, RNG tail / join, attention kernel) ms of the last step."""
+        arr = (C.c_float * 3)()
+        _lib.check(_lib.lib().rgo_block_last_timings3(self.handle, arr))
+        return float(arr[0]), float(arr[1]), float(arr[2])
 
     def close(self):
         if getattr(self, "handle", None):

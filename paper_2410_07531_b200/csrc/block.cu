@@ -139,7 +139,9 @@ struct Block {
     cudaStream_t s_main = nullptr, s_rng = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_rng = nullptr;  // fork/join inside a step
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;    // ordering against the caller's stream
-    cudaEvent_t ev_t[3] = {nullptr, nullptr, nullptr}; // phase timing (recorded inside the graph)
+    // phase timing (recorded inside the graph): [0] step start, [1] after the GEMM
+    // window, [2] after the end of the step, [3] right before the attention kernel
+    cudaEvent_t ev_t[4] = {nullptr, nullptr, nullptr, nullptr};
     // chunked pipeline: per chunk "mask c ready" (s_rng) and "slot of c free" (s_main)
     static constexpr int MAX_CHUNKS = 64;
     cudaEvent_t ev_chunk[MAX_CHUNKS] = {}, ev_slot[MAX_CHUNKS] = {};
@@ -278,6 +280,7 @@ static cudaError_t enqueue_step(Block& b, int* launches) {
     } else if (b.mode == BLOCK_STREAMS) {
         if ((e = cudaStreamWaitEvent(s, b.ev_rng, 0)) != cudaSuccess) return e;
     }
+    if ((e = record_timing(b, 3, s)) != cudaSuccess) return e;
     // attention on the QKV GEMM output (token-major [M, 3d]) -> attn_o [M, d]
     AttnJob a{};
     a.B = c.batch; a.H = c.heads; a.S = c.seq; a.HD = c.head_dim;
@@ -375,6 +378,7 @@ static cudaError_t enqueue_step_chunked(Block& b, int* launches) {
         ++n;
         if (ch == C - 1 && (e = record_timing(b, 1, s)) != cudaSuccess) return e;
         if (b.mode == BLOCK_STREAMS && (e = cudaStreamWaitEvent(s, b.ev_chunk[ch], 0)) != cudaSuccess) return e;
+        if (ch == C - 1 && (e = record_timing(b, 3, s)) != cudaSuccess) return e;
         AttnJob a{};
         a.B = Bc; a.H = c.heads; a.S = c.seq; a.HD = c.head_dim;
         a.scale = 1.0f / sqrtf(static_cast<float>(c.head_dim));
@@ -416,7 +420,7 @@ cudaError_t block_create(const BlockConfig& cfg, const BlockBuffers& buf, int mo
     if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&b->s_rng, cudaStreamNonBlocking, lo);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&b->ev_fork, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&b->ev_rng, cudaEventDisableTiming);
-    for (int t = 0; t < 3 && e == cudaSuccess; ++t) e = cudaEventCreate(&b->ev_t[t]);
+    for (int t = 0; t < 4 && e == cudaSuccess; ++t) e = cudaEventCreate(&b->ev_t[t]);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&b->ev_in, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&b->ev_out, cudaEventDisableTiming);
     if (cfg.chunks > Block::MAX_CHUNKS) e = cudaErrorInvalidValue;
@@ -469,13 +473,21 @@ cudaError_t block_last_timings(Block* b, float* ms2) {
     return e;
 }
 
+cudaError_t block_last_timings3(Block* b, float* ms3) {
+    cudaError_t e = cudaEventSynchronize(b->ev_t[2]);
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&ms3[0], b->ev_t[0], b->ev_t[1]);
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&ms3[1], b->ev_t[1], b->ev_t[3]);
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&ms3[2], b->ev_t[3], b->ev_t[2]);
+    return e;
+}
+
 void block_destroy(Block* b) {
     if (!b) return;
     if (b->exec) cudaGraphExecDestroy(b->exec);
     if (b->graph) cudaGraphDestroy(b->graph);
     if (b->ev_fork) cudaEventDestroy(b->ev_fork);
     if (b->ev_rng) cudaEventDestroy(b->ev_rng);
-    for (int t = 0; t < 3; ++t)
+    for (int t = 0; t < 4; ++t)
         if (b->ev_t[t]) cudaEventDestroy(b->ev_t[t]);
     if (b->ev_in) cudaEventDestroy(b->ev_in);
     if (b->ev_out) cudaEventDestroy(b->ev_out);

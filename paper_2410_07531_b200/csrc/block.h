@@ -54,6 +54,8 @@ cudaError_t block_step(Block* b, cudaStream_t stream, int* launches);
 // Device time of the last step's phases: [0] GEMM window (quant + 4 GEMMs),
 // [1] attention (incl. the RNG join / tail), in ms.
 cudaError_t block_last_timings(Block* b, float* ms2);
+// [0] GEMM window, [1] RNG tail / join before the attention, [2] attention kernel.
+cudaError_t block_last_timings3(Block* b, float* ms3);
 void block_destroy(Block* b);
 cudaError_t launch_quant_e4m3(const void* in, void* out, uint64_t n, float scale, cudaStream_t s);
 

@@ -507,6 +507,12 @@ int rgo_block_last_timings(rgo_block* blk, float* ms2) {
     return ce == cudaSuccess ? RGO_OK : cuda_fail(ce, "rgo_block_last_timings");
 }
 
+int rgo_block_last_timings3(rgo_block* blk, float* ms3) {
+    if (!blk || !ms3) return fail(RGO_EINVAL, "rgo_block_last_timings3: null argument");
+    cudaError_t ce = rgo::block_last_timings3(blk->impl, ms3);
+    return ce == cudaSuccess ? RGO_OK : cuda_fail(ce, "rgo_block_last_timings3");
+}
+
 int rgo_block_destroy(rgo_block* blk) {
     if (!blk) return RGO_OK;
     rgo::block_destroy(blk->impl);
