@@ -386,8 +386,8 @@ def bench_block(args, rank, world):
     mask_ms = max_over_ranks(mask_ms, world)
     best, value, summ = block_summary(rgo, wl, res, phases, mask_ms, peaks)
     # ----- e2e through the public API with host buffers.  A step's input is the
-    # previous attention output (bf16 [M, d], 128 MiB, read by the step's first
-    # kernel); every timed step copies a fresh one from pinned host memory and
+    # previous block's attention output (`attn_in`, bf16 [M, d], 128 MiB, read by the
+    # step's first kernel); every timed step copies a fresh one from pinned host memory and
     # reads back a row block of its result.  Two block replicas alternate so the
     # next step's 128 MiB H2D (copy stream) overlaps the current step, as a
     # serving loop would do.
@@ -397,7 +397,7 @@ def bench_block(args, rank, world):
     b2 = rgo.Block(wl, best, seed=42, base_offset=b.desc.base_offset, weights=b.weights,
                    rng_launch=(tuple(args.rng_launch) if best == "streams" else (0, args.rng_warps, 0)))
     pair = (b, b2)
-    host_in = [t.cpu().pin_memory() for t in (b.attn_o, (b.attn_o.float() * 0.5).bfloat16())]
+    host_in = [t.cpu().pin_memory() for t in (b.attn_in, (b.attn_in.float() * -1.0).bfloat16())]
     out_host = torch.empty(4096, dtype=torch.bfloat16).pin_memory()
     copy_stream = torch.cuda.Stream()
     ev_in = [torch.cuda.Event() for _ in range(2)]
@@ -407,7 +407,7 @@ def bench_block(args, rank, world):
     def stage_input(slot, k):
         with torch.cuda.stream(copy_stream):
             copy_stream.wait_event(ev_done[slot])
-            pair[slot].attn_o.copy_(host_in[k % 2], non_blocking=True)
+            pair[slot].attn_in.copy_(host_in[k % 2], non_blocking=True)
             ev_in[slot].record(copy_stream)
 
     for slot in range(2):

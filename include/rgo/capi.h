@@ -299,6 +299,7 @@ typedef struct rgo_block_buffers {
     float* lse;     /* optional [B*nH*S] */
     void* xd;       /* MoE: e4m3 [M*top_k, d] dispatched expert inputs (NULL when dense) */
     void* ye;       /* MoE: bf16 [M*top_k, d] expert outputs (NULL when dense) */
+    const void* attn_in; /* bf16 [M, d] step input; NULL = attn_o (steps chained through it) */
 } rgo_block_buffers;
 
 typedef struct rgo_block rgo_block;

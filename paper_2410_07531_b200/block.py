@@ -30,9 +30,14 @@ class Block:
     """Owns the device buffers of one block replica and the C-ABI handle."""
 
     def __init__(self, cfg: WorkloadConfig, mode: str = "streams", seed: int = 42, base_offset: int = 0,
-                 rng_launch=(0, 0, 0), use_graph: bool = True, device="cuda", weights=None, chunks: int = 1):
+                 rng_launch=(0, 0, 0), use_graph: bool = True, device="cuda", weights=None, chunks: int = 1,
+                 chained: bool = False):
         """chunks > 1: pipeline the step over `chunks` batch groups (schedule.hpp:206-239);
-        the mask buffer is then a 2-slot ring of chunk masks."""
+        the mask buffer is then a 2-slot ring of chunk masks.  chained=False (default):
+        every step reads the same stationary input `attn_in` (unit-variance synthetic
+        data); chained=True: each step consumes the previous step's attention output,
+        which -- without the LayerNorm/residuals the reference also omits -- drifts to
+        the e4m3 saturation limit over many steps."""
         import torch
         self.cfg, self.mode = cfg, mode
         B, S, H, D = cfg.batch, cfg.seq, cfg.heads, cfg.head_dim
@@ -47,7 +52,8 @@ class Block:
         self.weights = weights
         self.x = _uniform(M * d, 8, seed, dev).view(M, d).to(f8)
         self.qkv = torch.empty(M, 3 * d, dtype=bf, device=dev)
-        self.attn_o = (_uniform(M * d, 9, seed, dev).view(M, d) * 0.1).to(bf)
+        self.attn_in = _uniform(M * d, 9, seed, dev).view(M, d).mul_(math.sqrt(3.0)).to(bf)  # unit variance
+        self.attn_o = self.attn_in.clone() if chained else torch.empty(M, d, dtype=bf, device=dev)
         self.attn_o8 = torch.empty(M, d, dtype=f8, device=dev)
         self.y1 = torch.empty(M, d, dtype=f8, device=dev)
         E, k = cfg.experts, cfg.top_k
@@ -72,7 +78,8 @@ class Block:
             torch.cuda.synchronize()
         self.counter = torch.zeros(1, dtype=torch.int64, device=dev)
         self.lse = None
-        ku = 3.0  # E[(U(-1,1))^2] = 1/3 -> alpha = 3/sqrt(K) gives unit-variance outputs
+        # weights U(-1,1) (variance 1/3): alpha = sqrt(3/K) keeps activations at unit
+        # variance; a chained step's input is an attention output (~0.1-0.3): s_attn 8
         desc = _lib.block_desc()
         desc.batch, desc.seq, desc.heads, desc.head_dim, desc.ffn = B, S, H, D, F
         desc.gated = 1 if cfg.gated else 0
@@ -80,9 +87,9 @@ class Block:
         desc.rounds = cfg.philox_rounds
         desc.use_graph = 1 if use_graph else 0
         desc.seed, desc.base_offset = seed, base_offset
-        desc.a_qkv, desc.a_proj = ku / math.sqrt(d), ku / math.sqrt(d)
-        desc.a_ffn1, desc.a_ffn2 = ku / math.sqrt(d), ku / math.sqrt(F)
-        desc.s_attn, desc.s_proj, desc.s_ffn1, desc.s_ffn2 = 8.0, 1.0, 2.0, 1.0
+        desc.a_qkv, desc.a_proj = math.sqrt(3.0 / d), math.sqrt(3.0 / d)
+        desc.a_ffn1, desc.a_ffn2 = math.sqrt(3.0 / d), math.sqrt(3.0 / F)
+        desc.s_attn, desc.s_proj, desc.s_ffn1, desc.s_ffn2 = (8.0 if chained else 1.0), 1.0, 2.0, 1.0
         desc.rng_launch = _lib.launch(*rng_launch, 0)
         desc.experts, desc.top_k = (E, k) if E else (0, 0)
         desc.chunks = self.chunks
@@ -92,7 +99,8 @@ class Block:
                                   w["w2"].data_ptr(), self.qkv.data_ptr(), self.attn_o.data_ptr(),
                                   self.attn_o8.data_ptr(), self.y1.data_ptr(), self.h.data_ptr(),
                                   self.mask.data_ptr(), self.mask.numel(), self.counter.data_ptr(), None,
-                                  self.xd.data_ptr() if E else None, self.ye.data_ptr() if E else None)
+                                  self.xd.data_ptr() if E else None, self.ye.data_ptr() if E else None,
+                                  None if chained else self.attn_in.data_ptr())
         self._bufs = bufs
         handle = C.c_void_p()
         torch.cuda.synchronize()

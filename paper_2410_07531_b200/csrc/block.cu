@@ -218,7 +218,8 @@ static cudaError_t enqueue_step(Block& b, int* launches) {
     const RngQueue* rq = b.mode == BLOCK_IN_GEMM ? &q : nullptr;
     if ((e = record_timing(b, 0, s)) != cudaSuccess) return e;
     // attention output of the previous block -> e4m3
-    if ((e = launch_quant_e4m3(x.attn_o, x.attn_o8, static_cast<uint64_t>(M) * d, c.s_attn, s)) != cudaSuccess)
+    if ((e = launch_quant_e4m3(x.attn_in ? x.attn_in : x.attn_o, x.attn_o8, static_cast<uint64_t>(M) * d, c.s_attn,
+                               s)) != cudaSuccess)
         return e;
     ++n;
     GemmJob g;
@@ -355,7 +356,7 @@ static cudaError_t enqueue_step_chunked(Block& b, int* launches) {
             if ((e = cudaEventRecord(b.ev_chunk[ch], b.s_rng)) != cudaSuccess) return e;
         }
         const int r0 = ch * Mc;
-        const uint8_t* ao = static_cast<const uint8_t*>(x.attn_o) + static_cast<uint64_t>(r0) * d * 2;
+        const uint8_t* ao = static_cast<const uint8_t*>(x.attn_in ? x.attn_in : x.attn_o) + static_cast<uint64_t>(r0) * d * 2;
         uint8_t* ao8 = static_cast<uint8_t*>(x.attn_o8) + static_cast<uint64_t>(r0) * d;
         if ((e = launch_quant_e4m3(ao, ao8, static_cast<uint64_t>(Mc) * d, c.s_attn, s)) != cudaSuccess) return e;
         ++n;

@@ -46,6 +46,8 @@ struct BlockBuffers {
     float* lse;     // optional [B*nH*S]
     void* xd;       // MoE: e4m3 [M*top_k, d] expert-sorted (dispatched) FFN inputs
     void* ye;       // MoE: bf16 [M*top_k, d] expert FFN outputs before the combine
+    const void* attn_in;  // bf16 [M, d] step input (previous block's attention output);
+                          // null: attn_o, i.e. each step consumes the previous step's output
 };
 
 struct Block;

@@ -485,7 +485,7 @@ int rgo_block_create(const rgo_block_desc* d, const rgo_block_buffers* b, int32_
     c.top_k = static_cast<int>(d->top_k);
     c.chunks = static_cast<int>(chunks);
     rgo::BlockBuffers bb{b->x, b->wqkv, b->wo, b->w1, b->w2, b->qkv, b->attn_o, b->attn_o8, b->y1, b->h,
-                         b->mask, b->mask_bytes, b->counter, b->lse, b->xd, b->ye};
+                         b->mask, b->mask_bytes, b->counter, b->lse, b->xd, b->ye, b->attn_in};
     rgo::Block* impl = nullptr;
     cudaError_t ce = rgo::block_create(c, bb, mode, d->use_graph != 0, &impl);
     if (ce != cudaSuccess) return cuda_fail(ce, "rgo_block_create");

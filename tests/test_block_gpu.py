@@ -48,7 +48,7 @@ def test_block_stages_vs_torch(rgo, cuda):
     import torch.nn.functional as F
     cfg = small_cfg(rgo)
     b = rgo.Block(cfg, "streams", seed=7)
-    attn_in = b.attn_o.clone()
+    attn_in = b.attn_in.clone()
     b.step()
     torch.cuda.synchronize()
     d, Fd = b.d, b.F
@@ -81,8 +81,8 @@ def test_block_stages_vs_torch(rgo, cuda):
 def test_graph_replay_is_deterministic(rgo, cuda):
     import torch
     cfg = small_cfg(rgo)
-    b1 = rgo.Block(cfg, "streams", seed=3, use_graph=True)
-    b2 = rgo.Block(cfg, "streams", seed=3, use_graph=False)
+    b1 = rgo.Block(cfg, "streams", seed=3, use_graph=True, chained=True)
+    b2 = rgo.Block(cfg, "streams", seed=3, use_graph=False, chained=True)
     for _ in range(3):
         b1.step()
         b2.step()
