@@ -596,8 +596,8 @@ def main():
     ap.add_argument("--rounds", type=int, default=10)
     ap.add_argument("--rng-launch", type=int, nargs=3, default=[0, 0, 0], metavar=("GRID", "BLOCK", "SMEM"),
                     help="mechanism A mask-kernel launch shape (0 = one 256-thread CTA per SM)")
-    ap.add_argument("--rng-warps", type=int, default=8, choices=[4, 6, 8],
-                    help="mechanism B: RNG warps co-resident in each GEMM CTA")
+    ap.add_argument("--rng-warps", type=int, default=0, choices=[0, 4, 6, 8, 12, 16],
+                    help="mechanism B: RNG warps co-resident in each GEMM CTA (0 = the block's per-workload choice)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true",
                     help="skip the secondary configs (GPT-3 block, attention fwd+bwd, SQ sweep)")

@@ -166,6 +166,22 @@ static GemmJob gemm(const BlockConfig& c, int M, int N, int K, const void* A, co
     return j;
 }
 
+// Mechanism B's RNG warps per GEMM CTA when the caller leaves the choice to the
+// block (rng_block = 0): scaled with the mask's Philox work per GEMM flop.  On the
+// power-capped part more RNG warps barely lengthen the GEMM window but shrink the
+// tail drain (scripts/diag/block_phases.py, realistic data, modes interleaved):
+// Llama2-7B (3.2e-4 elements/flop) 8 -> 12 warps: tail 0.41 -> 0.22 ms, step
+// 4.12 -> 3.96 ms (16: 0.12 ms tail, same step); MoE (1.6e-4) and GPT-3 (0.5e-4,
+// Philox-7) leave no tail at 8 and 12/16 only cost GEMM issue slots.
+static int auto_rng_warps(const BlockConfig& c) {
+    const double M = static_cast<double>(c.batch) * c.seq, d = static_cast<double>(c.heads) * c.head_dim;
+    const double rows_ffn = c.experts > 0 ? M * c.top_k : M;
+    const double flops = 2.0 * M * d * 4.0 * d + 2.0 * rows_ffn * d * c.ffn * ((c.gated ? 2 : 1) + 1);
+    const double work = static_cast<double>(c.batch) * c.heads * c.seq * static_cast<double>(c.seq) * c.rounds / 10.0;
+    const double r = work / flops;
+    return r <= 2.0e-4 ? 8 : (r <= 3.5e-4 ? 12 : 16);
+}
+
 // Phase-timing events: inside a graph capture they must be external event
 // record nodes; in eager mode a plain record.
 static cudaError_t record_timing(Block& b, int i, cudaStream_t s) {
@@ -225,7 +241,8 @@ static cudaError_t enqueue_step(Block& b, int* launches) {
     GemmJob g;
     g = gemm(c, M, d, d, x.attn_o8, x.wo, x.y1, rgo_gk::EPI_NONE, rgo_gk::OUT_E4M3, c.a_proj, c.s_proj);
     g.rng = rq;
-    const int rw = static_cast<int>(c.rng_block);  // IN_GEMM: RNG warps per GEMM CTA (0 = default)
+    // IN_GEMM: RNG warps per GEMM CTA (4, 6, 8, 12 or 16; 0 = auto_rng_warps)
+    const int rw = c.rng_block ? static_cast<int>(c.rng_block) : auto_rng_warps(c);
     g.rng_warps = rw;
     if ((e = launch_gemm(g, s)) != cudaSuccess) return e;
     ++n;

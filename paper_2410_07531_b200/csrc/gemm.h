@@ -41,7 +41,7 @@ struct GemmJob {
     float out_scale;         // pre-cast multiplier (fp8 output quantisation)
     int grid;                // 0 = #SMs (persistent)
     const RngQueue* rng;     // non-null: co-resident RNG warps drain this queue
-    int rng_warps;           // 4, 6 or 8 (0 = RNG_WARPS_IN_GEMM; 8 measured best, 12 slower)
+    int rng_warps;           // 4, 6, 8, 12 or 16 (0 = RNG_WARPS_IN_GEMM; the block picks per workload)
 };
 
 cudaError_t launch_gemm(const GemmJob& j, cudaStream_t s);

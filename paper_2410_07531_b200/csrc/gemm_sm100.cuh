@@ -310,6 +310,8 @@ cudaError_t launch_variant(const CUtensorMap& ta, const CUtensorMap& tb, const P
     if (!rng) return launch_t<F, E, O, 0>(ta, tb, p, grid, s);
     if (rw == 6) return launch_t<F, E, O, 6>(ta, tb, p, grid, s);
     if (rw == 8) return launch_t<F, E, O, 8>(ta, tb, p, grid, s);
+    if (rw == 12) return launch_t<F, E, O, 12>(ta, tb, p, grid, s);
+    if (rw == 16) return launch_t<F, E, O, 16>(ta, tb, p, grid, s);
     return launch_t<F, E, O, 4>(ta, tb, p, grid, s);
 }
 

@@ -43,6 +43,25 @@ def test_modes_bitwise_identical(rgo, cuda):
         assert torch.equal(outs[mode][1], want[: outs[mode][1].numel()]), mode
 
 
+@pytest.mark.parametrize("warps", [4, 6, 8, 12, 16])
+def test_in_gemm_rng_warp_counts(rgo, cuda, warps):
+    """Mechanism B with each co-resident RNG-warp count: K1's mask, the
+    serial-fused block's outputs."""
+    import torch
+    cfg = small_cfg(rgo)
+    ref = rgo.Block(cfg, "serial_fused", seed=42)
+    ref.step()
+    b = rgo.Block(cfg, "in_gemm", seed=42, rng_launch=(0, warps, 0))
+    b.step()
+    torch.cuda.synchronize()
+    for k, v in snapshot(b).items():
+        assert torch.equal(v.view(torch.uint8), getattr(ref, k).view(torch.uint8)), k
+    want = rgo.generate_mask_device(rgo.MaskLayout(cfg.batch, cfg.heads, cfg.seq, 42), rgo.KeepThreshold(0.9), 10)
+    assert torch.equal(b.mask, want[: b.mask.numel()])
+    ref.close()
+    b.close()
+
+
 def test_block_stages_vs_torch(rgo, cuda):
     import torch
     import torch.nn.functional as F
