@@ -180,7 +180,8 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(const __grid_const
     uint64_t* s_full = v_empty + KV_STAGES;  // [2]
     uint64_t* p_full = s_full + 2;           // [2]
     uint64_t* o_done = p_full + 2;           // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
+    uint64_t* p_half = o_done + 2;           // [2] first 64 P columns in TMEM
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_half + 2);
 
     const uint32_t warp = warp_id(), lane = lane_id();
     const int pair = blockIdx.x % p.n_pairs;
@@ -201,6 +202,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(const __grid_const
             mbar_init(smem_u32(&s_full[w]), 1);
             mbar_init(smem_u32(&p_full[w]), 4);
             mbar_init(smem_u32(&o_done[w]), 1);
+            mbar_init(smem_u32(&p_half[w]), 4);
         }
         fence_mbar_init();
         tma_prefetch_desc(&tmQ);
@@ -262,9 +264,11 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(const __grid_const
                                k_desc + ((ks * SM::TILE) >> 4) + off, IDESC_S, kk > 0);
                 }
             };
-            auto issue_o = [&](int w, int vs, bool acc) {
+            // O += P.V in two K halves: keys [0,64) as soon as the softmax warps
+            // have written the first 64 P columns (p_half), keys [64,128) after p_full
+            auto issue_o = [&](int w, int vs, bool acc, int k_lo, int k_hi) {
 #pragma unroll
-                for (int kk = 0; kk < BKV / 16; ++kk)
+                for (int kk = k_lo; kk < k_hi; ++kk)
                     mma_f16_ts(tmem + 256 + w * 128, tmem + w * 128 + kk * 8,
                                v_desc + ((vs * SM::TILE + kk * 2048) >> 4), IDESC_O, (acc || kk > 0) ? 1u : 0u);
             };
@@ -288,10 +292,14 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(const __grid_const
                 if (has_next) mbar_wait(smem_u32(&k_full[ks]), kph);
                 tc_fence_after();
                 for (int w = 0; w < 2; ++w) {
+                    mbar_wait(smem_u32(&p_half[w]), j & 1);
+                    tc_fence_after();
+                    if (elect_one()) issue_o(w, vs, j > 0, 0, BKV / 32);
+                    __syncwarp();
                     mbar_wait(smem_u32(&p_full[w]), j & 1);
                     tc_fence_after();
                     if (elect_one()) {
-                        issue_o(w, vs, j > 0);
+                        issue_o(w, vs, true, BKV / 32, BKV / 16);
                         if (has_next) {
                             issue_s(w, ks);
                             tc_commit(smem_u32(&s_full[w]));
@@ -417,6 +425,12 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(const __grid_const
                     }
                 }
                 tmem_st32(tS + 32 * h, pk);
+                if (h == 0) {
+                    tmem_st_wait();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(smem_u32(&p_half[w]));
+                }
             }
             const float rs = rs2.x + rs2.y;
             l += rs;
