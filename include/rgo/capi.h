@@ -134,7 +134,7 @@ typedef struct rgo_gemm_desc {
     float alpha;        /* dequantisation scale of A.B (sa * sb) */
     float out_scale;    /* multiplier before the output cast */
     int32_t grid;       /* 0 = one persistent CTA per SM */
-    int32_t reserved;
+    int32_t rng_warps;  /* rgo_gemm_with_rng: co-resident RNG warps per CTA, 4/6/8/12/16 (0 = 8) */
 } rgo_gemm_desc;
 
 int rgo_gemm(const rgo_gemm_desc* g, const void* d_a, const void* d_b, void* d_c,

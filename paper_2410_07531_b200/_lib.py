@@ -54,7 +54,7 @@ class gemm_desc(C.Structure):
         ("in_dtype", C.c_int32), ("out_dtype", C.c_int32), ("epilogue", C.c_int32),
         ("lda", C.c_int64), ("ldb", C.c_int64), ("ldc", C.c_int64),
         ("alpha", C.c_float), ("out_scale", C.c_float),
-        ("grid", C.c_int32), ("reserved", C.c_int32),
+        ("grid", C.c_int32), ("rng_warps", C.c_int32),
     ]
 
 

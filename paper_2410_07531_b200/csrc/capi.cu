@@ -294,6 +294,10 @@ static int gemm_job(const rgo_gemm_desc* g, const void* a, const void* b, void* 
     j->epi = g->epilogue;
     j->out = g->out_dtype == RGO_DT_E4M3 ? rgo_gk::OUT_E4M3 : rgo_gk::OUT_BF16;
     j->alpha = g->alpha; j->out_scale = g->out_scale; j->grid = g->grid; j->rng = nullptr;
+    const int rw = g->rng_warps;
+    if (rw != 0 && rw != 4 && rw != 6 && rw != 8 && rw != 12 && rw != 16)
+        return fail(RGO_EINVAL, "gemm: rng_warps must be 0, 4, 6, 8, 12 or 16 (got %d)", rw);
+    j->rng_warps = rw;
     return RGO_OK;
 }
 

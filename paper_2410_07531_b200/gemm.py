@@ -125,11 +125,14 @@ def gemm(a, b, c=None, *, alpha: float = 1.0, out_scale: float = 1.0, epilogue: 
 
 
 def gemm_with_rng(a, b, c, mask_desc: _lib.mask_desc, bits, counter, *, alpha: float = 1.0,
-                  out_scale: float = 1.0, epilogue: str = "none", grid: int = 0, stream=None):
-    """K4: gemm() with co-resident RNG warps draining the mask queue."""
+                  out_scale: float = 1.0, epilogue: str = "none", grid: int = 0, rng_warps: int = 0,
+                  stream=None):
+    """K4: gemm() with co-resident RNG warps (rng_warps per CTA: 4/6/8/12/16, 0 = 8)
+    draining the mask queue."""
     import torch
     s = (stream or torch.cuda.current_stream()).cuda_stream
     d = gemm_desc(a, b, c, alpha, out_scale, epilogue, grid)
+    d.rng_warps = rng_warps
     _lib.check(_lib.lib().rgo_gemm_with_rng(d, a.data_ptr(), b.data_ptr(), c.data_ptr(), mask_desc,
                                             bits.data_ptr(), bits.numel(), counter.data_ptr(), s))
     return c

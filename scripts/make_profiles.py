@@ -21,7 +21,8 @@ lines = [f"# {RND}: ncu --set full, one launch per hot kernel (B200, Llama2-7B s
          "one GPU), reduced by `scripts/make_profiles.py`. Per-launch times under ncu are cold-cache and",
          "serialised: compare shares, not absolutes.", ""]
 for k, title in (("mask", "K1 rng_mask_kernel<10> (2^31 elements)"), ("gemm", "K2 FP8 GEMM FFN1 SwiGLU 16384x22016x4096"),
-                 ("gemm_rng", "K4 FP8 GEMM FFN1 + 8 co-resident RNG warps"),
+                 ("gemm_rng", "K4 FP8 GEMM FFN1 + co-resident RNG warps (12 per CTA, the Llama2-7B block's count)"),
+                 ("gemm_rng16", "K4 FP8 GEMM FFN1 + 16 co-resident RNG warps per CTA"),
                  ("attn_bits", "K5 attention fwd, mask bits (B4 H32 S4096 D128)"),
                  ("attn_philox", "K6 attention fwd, inline Philox-10"),
                  ("bwd_bits", "K7 attention bwd, mask bits (B4 H32 S4096 D128)"),

@@ -57,6 +57,7 @@ if which == "gemm_rng":
     counter = torch.zeros(1, dtype=torch.int64, device="cuda")
     for _ in range(3):
         counter.zero_()
-        rgo.gemm_with_rng(a, b, c, d, bits, counter, epilogue="swiglu", alpha=0.05)
+        rgo.gemm_with_rng(a, b, c, d, bits, counter, epilogue="swiglu", alpha=0.05,
+                          rng_warps=int(os.environ.get("RNG_WARPS", "0")))
     torch.cuda.synchronize()
     print("rng vectors done during one GEMM:", int(counter.item()), "of", lay.elem_count() // 128)

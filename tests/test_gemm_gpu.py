@@ -66,7 +66,8 @@ def test_gelu_epilogue_fp8_out(rgo, cuda):
     assert rel(c.float(), ref.to(torch.float8_e4m3fn).float()) < 2e-2
 
 
-def test_gemm_with_rng_mask_and_output(rgo, cuda):
+@pytest.mark.parametrize("warps", [0, 4, 12, 16])
+def test_gemm_with_rng_mask_and_output(rgo, cuda, warps):
     """K4: co-resident RNG warps leave the GEMM result unchanged and, with the
     tail drain, produce the K1 mask bit-exactly."""
     import torch
@@ -78,7 +79,7 @@ def test_gemm_with_rng_mask_and_output(rgo, cuda):
     counter = torch.zeros(1, dtype=torch.int64, device="cuda")
     c0 = rgo.gemm(a, b)
     c1 = torch.empty_like(c0)
-    rgo.gemm_with_rng(a, b, c1, d, bits, counter)
+    rgo.gemm_with_rng(a, b, c1, d, bits, counter, rng_warps=warps)
     torch.testing.assert_close(c1, c0, rtol=0, atol=0)
     rgo.mask_queue_drain(d, bits, counter)
     want = rgo.generate_mask_device(lay, thr, 10)
@@ -103,3 +104,11 @@ def test_gemm_validation(rgo, cuda):
     b = torch.zeros(256, 100, dtype=torch.bfloat16, device="cuda")
     with pytest.raises(ValueError):
         rgo.gemm(a, b)  # k*2 not a multiple of 128 bytes
+    a = torch.zeros(128, 128, dtype=torch.bfloat16, device="cuda")
+    b = torch.zeros(256, 128, dtype=torch.bfloat16, device="cuda")
+    c = rgo.gemm(a, b)
+    lay = rgo.MaskLayout(1, 1, 128, 1)
+    bits = torch.zeros(lay.elem_count() // 8, dtype=torch.uint8, device="cuda")
+    counter = torch.zeros(1, dtype=torch.int64, device="cuda")
+    with pytest.raises(ValueError):
+        rgo.gemm_with_rng(a, b, c, rgo.mask.desc(lay, rgo.KeepThreshold(0.9), 10), bits, counter, rng_warps=5)
