@@ -273,7 +273,8 @@ typedef struct rgo_block_desc {
     uint64_t seed, base_offset;  /* mask layout of batch*heads slices */
     float a_qkv, a_proj, a_ffn1, a_ffn2;  /* FP8 dequant scales */
     float s_attn, s_proj, s_ffn1, s_ffn2; /* output quantisation scales */
-    rgo_launch rng_launch;  /* STREAMS: mask-kernel launch shape */
+    rgo_launch rng_launch;  /* STREAMS: mask-kernel launch shape; IN_GEMM: rng_launch.block =
+                               RNG warps per GEMM CTA (4/6/8/12/16, 0 = chosen per workload) */
     uint32_t experts;       /* 0: dense FFN; > 0: MoE with `experts` expert FFNs of width ffn */
     uint32_t top_k;         /* MoE: experts per token (balanced synthetic routing) */
     uint32_t chunks;        /* > 1: pipeline the step over `chunks` batch groups (dense FFN, modes

@@ -53,6 +53,7 @@
 
 #include "attn.h"
 #include "philox.cuh"
+#include "rgo_internal.h"
 #include "sm100_ptx.cuh"
 #include "tma_host.h"
 
@@ -1140,12 +1141,7 @@ template <int MODE, int R>
 static cudaError_t launch_main2(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
                                 const CUtensorMap& dO, const CUtensorMap& m, const Params& p, cudaStream_t s) {
     auto kern = bwd_main2_kernel<MODE, R>;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem2::ALLOC);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    if (cudaError_t e = rgo::ensure_dyn_smem(reinterpret_cast<const void*>(kern), Smem2::ALLOC); e != cudaSuccess) return e;
     const unsigned grid = static_cast<unsigned>(p.B) * p.H * p.n_kt;
     kern<<<grid, THREADS, Smem2::ALLOC, s>>>(q, k, v, dO, m, p);
     return cudaGetLastError();
@@ -1155,12 +1151,7 @@ template <int HD, int MODE, int R>
 static cudaError_t launch_main(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
                                const CUtensorMap& dO, const Params& p, cudaStream_t s) {
     auto kern = bwd_main_kernel<HD, MODE, R>;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<HD>::ALLOC);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    if (cudaError_t e = rgo::ensure_dyn_smem(reinterpret_cast<const void*>(kern), Smem<HD>::ALLOC); e != cudaSuccess) return e;
     const unsigned grid = static_cast<unsigned>(p.B) * p.H * p.n_kt;
     kern<<<grid, THREADS, Smem<HD>::ALLOC, s>>>(q, k, v, dO, p);
     return cudaGetLastError();

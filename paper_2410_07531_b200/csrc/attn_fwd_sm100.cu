@@ -473,12 +473,8 @@ template <int HD, int MODE, int R>
 static cudaError_t launch_t(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v, const AttnParams& p,
                             cudaStream_t s) {
     auto kern = attn_fwd_kernel<HD, MODE, R>;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<HD>::BYTES);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    if (cudaError_t e = rgo::ensure_dyn_smem(reinterpret_cast<const void*>(kern), Smem<HD>::BYTES); e != cudaSuccess)
+        return e;
     const unsigned grid = static_cast<unsigned>(p.B) * p.H * p.n_pairs;
     kern<<<grid, THREADS, Smem<HD>::BYTES, s>>>(q, k, v, p);
     return cudaGetLastError();

@@ -282,12 +282,8 @@ template <bool FP8, int EPI, int OUT, int RNG_WARPS>
 cudaError_t launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, int grid,
                             cudaStream_t s) {
     auto k = gemm_kernel<FP8, EPI, OUT, RNG_WARPS>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
+    if (cudaError_t e = rgo::ensure_dyn_smem(reinterpret_cast<const void*>(k), SMEM_BYTES); e != cudaSuccess)
+        return e;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(grid));
     cfg.blockDim = dim3(CORE_THREADS + 32 * RNG_WARPS);

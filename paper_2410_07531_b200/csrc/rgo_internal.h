@@ -5,6 +5,9 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <mutex>
+#include <set>
+#include <utility>
 
 namespace rgo {
 
@@ -23,6 +26,22 @@ struct MaskJob {
     uint64_t threshold;     // KeepThreshold::threshold(), in [0, 2^32]
     int rounds;             // [1,16]
 };
+
+// Kernel attributes are per device: set the dynamic shared-memory opt-in once
+// per (kernel, current device), so launches on a second GPU of the same
+// process do not skip it.  Thread-safe.
+inline cudaError_t ensure_dyn_smem(const void* kernel, int bytes) {
+    static std::mutex mu;
+    static std::set<std::pair<const void*, int>> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.count({kernel, dev})) return cudaSuccess;
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done.insert({kernel, dev});
+    return e;
+}
 
 int num_sms();
 int mask_kernel_occupancy(int rounds, int block, size_t dyn_smem);
