@@ -215,11 +215,11 @@ def bench_mask_kernel(rgo, cfg, rank, steps, warmup):
     return ms, elems
 
 
-def run_block_modes(rgo, wl, rank, world, args, modes, chunks=1):
+def run_block_modes(rgo, wl, rank, world, args, modes, chunks=1, passes=1):
     """Each mode: W warm-up steps, then exactly K timed steps bracketed by
     barrier + synchronize (CUDA events, max over ranks).  The modes are
-    measured twice, in opposite orders, and averaged, so the GPU's power /
-    clock state (the FP8 GEMMs run at the 1 kW cap) biases none of them."""
+    measured 2 x passes times, in alternating orders, and averaged, so the GPU's
+    power / clock state (the FP8 GEMMs run at the 1 kW cap) biases none of them."""
     import torch
     from paper_2410_07531_b200.sharding import replica_base_offset
     base = replica_base_offset(wl.batch, wl.heads, wl.seq, rank)  # disjoint Philox counters per rank
@@ -230,7 +230,7 @@ def run_block_modes(rgo, wl, rank, world, args, modes, chunks=1):
     stream = torch.cuda.current_stream()
     samples = {m: [] for m in modes}
     phases, launches = {}, {}
-    for order in (modes, modes[::-1]):
+    for order in [modes, modes[::-1]] * passes:
         for m in order:
             b = blocks[m]
             for _ in range(args.warmup):
@@ -378,7 +378,7 @@ def bench_block(args, rank, world):
     peaks, src = load_peaks()
     log("Llama2-7B block modes")
     with ClockSampler(torch.cuda.current_device()) as clk:
-        blocks, res, samples, phases, launches = run_block_modes(rgo, wl, rank, world, args, modes)
+        blocks, res, samples, phases, launches = run_block_modes(rgo, wl, rank, world, args, modes, passes=3)
     log("mask kernel")
     att_ms = phases["no_rng"][1]  # the mask-reading attention kernel alone, in situ
     clocks = clk.summary()
@@ -490,7 +490,7 @@ def bench_block(args, rank, world):
         log("GPT-3 block")
         g = rgo.workload_preset("gpt3")
         g.philox_rounds = args.rounds
-        gblocks, gres, _, gph, _ = run_block_modes(rgo, g, rank, world, args, modes)
+        gblocks, gres, _, gph, _ = run_block_modes(rgo, g, rank, world, args, modes, passes=2)
         for blk in gblocks.values():
             blk.close()
         del gblocks
@@ -505,7 +505,7 @@ def bench_block(args, rank, world):
         log("MoE block")
         mo = rgo.workload_preset("moe")
         mo.philox_rounds = args.rounds
-        mblocks, mres, _, mph, _ = run_block_modes(rgo, mo, rank, world, args, modes)
+        mblocks, mres, _, mph, _ = run_block_modes(rgo, mo, rank, world, args, modes, passes=2)
         for blk in mblocks.values():
             blk.close()
         del mblocks
