@@ -154,8 +154,8 @@ __device__ __forceinline__ float2 ex2_poly2(float x0, float x1) {
                        __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
 }
 // Pairs (of the 16 per 32-column chunk) whose 2^x runs on the FMA pipes: one
-// in POLY_EVERY (8: 12.5 %; 4 and 2 measured no better for the mask-bits kernel and
-// slower for the ALU-bound inline-Philox one).  MUFU.EX2 (16/clk/SM) and the tensor core need the same
+// in POLY_EVERY (8: 12.5 %; 4 is 0.5 % faster for the mask-bits kernel but slower for
+// the ALU-bound inline-Philox one, and K5 and K6 must share it to stay bitwise equal).  MUFU.EX2 (16/clk/SM) and the tensor core need the same
 // ~1024 cycles per 128x128 tile, so shifting a share to the idle FMA pipes
 // takes the softmax off the critical path.
 constexpr int POLY_EVERY = 8;
