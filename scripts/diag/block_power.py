@@ -1,6 +1,6 @@
 """Per block mode: run ~1.5 s of steps, sample nvidia-smi clocks/power at 20 ms (diagnostic)."""
 import json, os, subprocess, sys, time
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch
 import paper_2410_07531_b200 as rgo
 

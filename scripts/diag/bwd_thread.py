@@ -1,6 +1,6 @@
 """Diagnose attn_bwd from a non-main host thread (autograd worker)."""
 import sys, os, threading
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch
 import paper_2410_07531_b200 as rgo
 

@@ -1,6 +1,6 @@
 """GEMM slowdown when co-running pipe-specific spin kernels (diagnostic)."""
 import ctypes as C, json, os, sys
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch
 import paper_2410_07531_b200 as rgo
 

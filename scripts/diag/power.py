@@ -1,7 +1,7 @@
 """Diagnose GEMM/RNG co-run: per-kernel times alone vs concurrent, with
 nvidia-smi clocks/power sampled at 20 ms."""
 import json, os, subprocess, sys, threading, time
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch
 import paper_2410_07531_b200 as rgo
 

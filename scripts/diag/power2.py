@@ -1,7 +1,7 @@
 """Long back-to-back loops: GEMM alone, mask alone, both concurrently (two
 streams), with clocks/power sampled every 10 ms (diagnostic)."""
 import json, os, subprocess, sys, time
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch
 import paper_2410_07531_b200 as rgo
 
