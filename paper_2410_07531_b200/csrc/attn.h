@@ -52,6 +52,7 @@ struct AttnJob {
     uint64_t bits_bytes;
     uint64_t seed, base_offset, threshold;
     int rounds;
+    bool pdl;                // programmatic dependent launch after the previous kernel in the stream
 };
 
 cudaError_t launch_attn_fwd(const AttnJob& j, cudaStream_t s);

@@ -215,6 +215,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(const __grid_const
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     constexpr int NCH = HD / 64;
+    griddep_wait();  // launched as a programmatic dependent: the producers of Q/K/V and the mask are done
 
     if (warp < 4) {  // ---------------------------------------------- control warpgroup
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(CTRL_REGS));
@@ -471,13 +472,22 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(const __grid_const
 
 template <int HD, int MODE, int R>
 static cudaError_t launch_t(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v, const AttnParams& p,
-                            cudaStream_t s) {
+                            cudaStream_t s, bool pdl) {
     auto kern = attn_fwd_kernel<HD, MODE, R>;
     if (cudaError_t e = rgo::ensure_dyn_smem(reinterpret_cast<const void*>(kern), Smem<HD>::BYTES); e != cudaSuccess)
         return e;
     const unsigned grid = static_cast<unsigned>(p.B) * p.H * p.n_pairs;
-    kern<<<grid, THREADS, Smem<HD>::BYTES, s>>>(q, k, v, p);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = Smem<HD>::BYTES;
+    cfg.stream = s;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, q, k, v, p);
 }
 
 }  // namespace rgo_attn
@@ -519,7 +529,7 @@ cudaError_t launch_attn_fwd(const AttnJob& j, cudaStream_t s) {
     // keep-all (threshold 2^32) or keep_prob 1: every bit is 1 -> plain path, scale 1/p
     if (mode == MASK_PHILOX && j.threshold >= (uint64_t{1} << 32)) mode = MASK_NONE;
 #define RGO_A(HDV, MODEV, RV) \
-    if (j.HD == HDV && mode == MODEV) return launch_t<HDV, MODEV, RV>(tq, tk, tv, p, s);
+    if (j.HD == HDV && mode == MODEV) return launch_t<HDV, MODEV, RV>(tq, tk, tv, p, s, j.pdl);
     RGO_A(128, MASK_NONE, 0)
     RGO_A(64, MASK_NONE, 0)
     RGO_A(128, MASK_BITS, 0)

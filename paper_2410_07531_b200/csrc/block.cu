@@ -36,6 +36,7 @@ namespace rgo_dev {
 // bf16 -> e4m3 (saturating) with a scale; 16 elements per thread.
 __global__ void quant_e4m3_kernel(const __nv_bfloat16* __restrict__ in, uint8_t* __restrict__ out, uint64_t n,
                                   float scale) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the Proj GEMM may start its RNG warps
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x * 16;
     for (uint64_t i = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 16; i < n; i += stride) {
         if (i + 16 <= n) {
@@ -150,9 +151,18 @@ struct Block {
     int launches_per_step = 0;
 };
 
+static bool block_pdl() {  // RGO_BLOCK_PDL=0 turns programmatic dependent launch off (A/B)
+    static const bool on = [] {
+        const char* e = getenv("RGO_BLOCK_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 static GemmJob gemm(const BlockConfig& c, int M, int N, int K, const void* A, const void* B, void* C, int epi,
                     int out, float alpha, float out_scale) {
     GemmJob j{};
+    j.pdl = block_pdl();
     j.fp8 = true;
     j.M = M; j.N = N; j.K = K;
     j.A = A; j.lda = K; j.B = B; j.ldb = K;
@@ -293,7 +303,7 @@ static cudaError_t enqueue_step(Block& b, int* launches) {
     ++n;
     if ((e = record_timing(b, 1, s)) != cudaSuccess) return e;
     if (b.mode == BLOCK_IN_GEMM) {  // tail: whatever the GEMM-resident warps left
-        if ((e = launch_rng_queue(q, 0, 0, 0, s)) != cudaSuccess) return e;
+        if ((e = launch_rng_queue(q, 0, 0, 0, s, block_pdl())) != cudaSuccess) return e;
         ++n;
     } else if (b.mode == BLOCK_STREAMS) {
         if ((e = cudaStreamWaitEvent(s, b.ev_rng, 0)) != cudaSuccess) return e;
@@ -318,6 +328,9 @@ static cudaError_t enqueue_step(Block& b, int* launches) {
     a.base_offset = c.base_offset;
     a.threshold = c.threshold;
     a.rounds = c.rounds;
+    // programmatic dependent of the tail drain (IN_GEMM) or of the QKV GEMM (the other
+    // modes; in STREAMS mode an event join sits in between and the launch is a normal one)
+    a.pdl = block_pdl() && b.mode != BLOCK_STREAMS;
     if ((e = launch_attn_fwd(a, s)) != cudaSuccess) return e;
     ++n;
     if ((e = record_timing(b, 2, s)) != cudaSuccess) return e;
@@ -380,18 +393,22 @@ static cudaError_t enqueue_step_chunked(Block& b, int* launches) {
         GemmJob g;
         g = gemm(c, Mc, d, d, ao8, x.wo, const_cast<uint8_t*>(rows8(x.y1, r0, d)), rgo_gk::EPI_NONE, rgo_gk::OUT_E4M3,
                  c.a_proj, c.s_proj);
+        g.pdl = false;  // chunked: event joins between streams; kept on plain stream order
         if ((e = launch_gemm(g, s)) != cudaSuccess) return e;
         ++n;
         g = gemm(c, Mc, n1, d, rows8(x.y1, r0, d), x.w1, const_cast<uint8_t*>(rows8(x.h, r0, F)),
                  c.gated ? rgo_gk::EPI_SWIGLU : rgo_gk::EPI_GELU, rgo_gk::OUT_E4M3, c.a_ffn1, c.s_ffn1);
+        g.pdl = false;  // chunked: event joins between streams; kept on plain stream order
         if ((e = launch_gemm(g, s)) != cudaSuccess) return e;
         ++n;
         g = gemm(c, Mc, d, F, rows8(x.h, r0, F), x.w2, const_cast<uint8_t*>(rows8(x.x, r0, d)), rgo_gk::EPI_NONE,
                  rgo_gk::OUT_E4M3, c.a_ffn2, c.s_ffn2);
+        g.pdl = false;  // chunked: event joins between streams; kept on plain stream order
         if ((e = launch_gemm(g, s)) != cudaSuccess) return e;
         ++n;
         void* qkv_c = static_cast<uint8_t*>(x.qkv) + static_cast<uint64_t>(r0) * 3 * d * 2;
         g = gemm(c, Mc, 3 * d, d, rows8(x.x, r0, d), x.wqkv, qkv_c, rgo_gk::EPI_NONE, rgo_gk::OUT_BF16, c.a_qkv, 1.0f);
+        g.pdl = false;  // chunked: event joins between streams; kept on plain stream order
         if ((e = launch_gemm(g, s)) != cudaSuccess) return e;
         ++n;
         if (ch == C - 1 && (e = record_timing(b, 1, s)) != cudaSuccess) return e;

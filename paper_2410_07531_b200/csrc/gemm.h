@@ -42,10 +42,11 @@ struct GemmJob {
     int grid;                // 0 = #SMs (persistent)
     const RngQueue* rng;     // non-null: co-resident RNG warps drain this queue
     int rng_warps;           // 4, 6, 8, 12 or 16 (0 = RNG_WARPS_IN_GEMM; the block picks per workload)
+    bool pdl;                // programmatic dependent launch after the previous kernel in the stream
 };
 
 cudaError_t launch_gemm(const GemmJob& j, cudaStream_t s);
 cudaError_t launch_rng_queue(const RngQueue& q, unsigned grid, unsigned block, size_t dyn_smem,
-                             cudaStream_t s);
+                             cudaStream_t s, bool pdl = false);
 
 }  // namespace rgo

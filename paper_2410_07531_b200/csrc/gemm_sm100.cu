@@ -74,6 +74,7 @@ cudaError_t launch_gemm(const GemmJob& j, cudaStream_t s) {
     p.n_out = j.epi == EPI_SWIGLU ? j.N / 2 : j.N;
     p.alpha = j.alpha;
     p.out_scale = j.out_scale;
+    p.pdl = j.pdl ? 1 : 0;
     if (j.rng) p.rng = *j.rng;
     const int tiles = p.tiles_m * p.tiles_n;
     int grid = j.grid > 0 ? j.grid : num_sms();

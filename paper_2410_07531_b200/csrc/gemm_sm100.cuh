@@ -41,6 +41,7 @@ struct Params {
     float out_scale;      // multiply before the output cast (fp8 quantisation)
     // co-resident RNG (mechanism B)
     rgo::RngQueue rng;
+    int pdl;              // launched as a programmatic dependent of the previous kernel
 };
 
 __device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, int& mb, int& nb) {
@@ -149,7 +150,12 @@ __global__ void __launch_bounds__(CORE_THREADS + 32 * RNG_WARPS, 1)
     const int bk_elems = FP8 ? BKB : BKB / 2;
     constexpr uint32_t IDESC = FP8 ? idesc_make(0, 0, TILE_M, BN, 0, 0) : idesc_make(1, 1, TILE_M, BN, 0, 0);
 
+    // The next kernel in the stream may launch its CTAs as SMs free up (its RNG
+    // warps start draining at once); every role that touches global memory
+    // written or read by the previous kernel waits for it first.
+    griddep_launch_dependents();
     if (warp == 0) {  // ---------------- TMA producer (whole warp loops, one lane issues)
+        griddep_wait();
         int stage = 0;
         uint32_t phase = 0;
         const uint32_t sa = smem_u32(smA), sb = smem_u32(smB), eb0 = smem_u32(&empty[0]);
@@ -212,6 +218,7 @@ __global__ void __launch_bounds__(CORE_THREADS + 32 * RNG_WARPS, 1)
             }
         }
     } else if (warp < CORE_THREADS / 32) {  // ---------------- epilogue warps 2..5 (both CTAs)
+        griddep_wait();
         const uint32_t q = hw_warp & 3;  // TMEM lane quarter = physical warp id % 4
         const int row_in_tile = static_cast<int>(rank) * BM + q * 32 + lane;
         uint32_t acc = 0, acc_phase = 0;
@@ -289,13 +296,15 @@ cudaError_t launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const Params&
     cfg.blockDim = dim3(CORE_THREADS + 32 * RNG_WARPS);
     cfg.dynamicSmemBytes = SMEM_BYTES;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = p.pdl ? 2 : 1;
     return cudaLaunchKernelEx(&cfg, k, ta, tb, p);
 }
 

@@ -213,13 +213,18 @@ cudaError_t launch_mask(const MaskJob& j, const LaunchShape& shape_in, cudaStrea
 namespace rgo_dev {
 template <int R>
 __global__ void __launch_bounds__(256) rng_queue_kernel(const rgo::RngQueue q) {
+    // As a programmatic dependent (block tail after the last GEMM): start draining
+    // while the GEMM's last CTAs finish, let the attention kernel launch early, and
+    // complete only after the GEMM has (so the attention sees the GEMM's output).
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     rgo::rng_drain_r<R>(q, nullptr, 0);
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 }  // namespace rgo_dev
 
 namespace rgo {
 cudaError_t launch_rng_queue(const RngQueue& q, unsigned grid, unsigned block, size_t dyn_smem,
-                             cudaStream_t s) {
+                             cudaStream_t s, bool pdl) {
     if (block == 0) block = 256;
     if (grid == 0) grid = static_cast<unsigned>(num_sms()) * 3;
     switch (q.rounds) {
@@ -232,7 +237,20 @@ cudaError_t launch_rng_queue(const RngQueue& q, unsigned grid, unsigned block, s
         cudaFuncSetAttribute(rgo_dev::rng_queue_kernel<R>,                           \
                              cudaFuncAttributePreferredSharedMemoryCarveout,         \
                              cudaSharedmemCarveoutMaxShared);                        \
-        rgo_dev::rng_queue_kernel<R><<<grid, block, dyn_smem, s>>>(q);               \
+        {                                                                            \
+            cudaLaunchConfig_t cfg{};                                                \
+            cudaLaunchAttribute at[1];                                               \
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;           \
+            at[0].val.programmaticStreamSerializationAllowed = 1;                    \
+            cfg.gridDim = dim3(grid);                                                \
+            cfg.blockDim = dim3(block);                                              \
+            cfg.dynamicSmemBytes = dyn_smem;                                         \
+            cfg.stream = s;                                                          \
+            cfg.attrs = at;                                                          \
+            cfg.numAttrs = pdl ? 1 : 0;                                              \
+            cudaError_t le = cudaLaunchKernelEx(&cfg, rgo_dev::rng_queue_kernel<R>, q); \
+            if (le != cudaSuccess) return le;                                        \
+        }                                                                            \
         break;
         RGO_CASE(1) RGO_CASE(2) RGO_CASE(3) RGO_CASE(4) RGO_CASE(5) RGO_CASE(6) RGO_CASE(7)
         RGO_CASE(8) RGO_CASE(9) RGO_CASE(10) RGO_CASE(11) RGO_CASE(12) RGO_CASE(13)

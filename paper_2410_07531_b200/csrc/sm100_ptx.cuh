@@ -243,6 +243,14 @@ __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const void* tmap,
         "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar), "r"(c0), "r"(c1)
         : "memory");
 }
+// Programmatic dependent launch: a dependent grid's CTAs may start while its
+// predecessor in the stream finishes; griddep_wait() blocks until that
+// predecessor has completed and its memory is visible (a no-op without PDL).
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc2(uint32_t dst_smem) {  // one warp in each CTA of the pair
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(dst_smem), "n"(kCols)
