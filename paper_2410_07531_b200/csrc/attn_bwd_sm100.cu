@@ -90,7 +90,6 @@ struct Params {
     void* dV;
     long long k_sb, k_sh, k_ss;  // dK strides (elements)
     long long v_sb, v_sh, v_ss;  // dV strides
-    int debug;                   // experiment switches (RGO_BWD_DEBUG), 0 in production
     int mask_tma;                // v2, MASK_BITS: the keep-bit tile arrives by TMA with Q (SQ % 128 == 0)
 };
 
@@ -628,7 +627,7 @@ __global__ void __launch_bounds__(THREADS, 1) bwd_main_kernel(const __grid_const
             fence_proxy_async_smem();
             named_bar_sync(1, 128);
             if (leader) {
-                if (!(p.debug & 1)) bulk_reduce_add_f32(gdst, stg_addr, HALF_BYTES);
+                bulk_reduce_add_f32(gdst, stg_addr, HALF_BYTES);
                 bulk_commit();
             }
         };
@@ -1125,8 +1124,7 @@ __global__ void __launch_bounds__(THREADS, 1) bwd_main2_kernel(const __grid_cons
             fence_proxy_async_smem();
             named_bar_sync(1, 128);
             if (leader) {
-                if (!(p.debug & 1))
-                    bulk_reduce_add_f32(p.dq_acc + dq2_tile_base(slice, n_qt, qtile(i)), smem_u32(stg), SM::STG_BYTES);
+                bulk_reduce_add_f32(p.dq_acc + dq2_tile_base(slice, n_qt, qtile(i)), smem_u32(stg), SM::STG_BYTES);
                 bulk_commit();
             }
         }
@@ -1176,16 +1174,8 @@ static bool tmap4(CUtensorMap* m, const AttnTensor& t, int B, int H, int S, int 
     return make_tmap(m, t.ptr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
-// Experiment switches, read once per process (not per call): RGO_BWD_DEBUG=1
-// skips the dQ reductions (timing only -- dQ is then wrong), RGO_BWD_V1=1
-// runs the 128-query-tile kernel for head_dim 128 as well.
-static int bwd_debug_flags() {
-    static const int v = [] {
-        const char* d = getenv("RGO_BWD_DEBUG");
-        return d ? atoi(d) : 0;
-    }();
-    return v;
-}
+// RGO_BWD_V1=1 (read once per process) runs the 128-query-tile kernel for head
+// dim 128 as well (the 64-query-tile kernel is faster there; same results).
 static bool bwd_force_v1() {
     static const bool v = getenv("RGO_BWD_V1") != nullptr;
     return v;
@@ -1211,7 +1201,6 @@ static void fill_params(rgo_attn_bwd::Params& p, const AttnBwdJob& j, int n_qt, 
     p.dq_acc = dq_acc;
     p.dK = j.dk.ptr; p.k_sb = j.dk.sb; p.k_sh = j.dk.sh; p.k_ss = j.dk.ss;
     p.dV = j.dv.ptr; p.v_sb = j.dv.sb; p.v_sh = j.dv.sh; p.v_ss = j.dv.ss;
-    p.debug = bwd_debug_flags();
 }
 
 // head_dim 128: the 64-query-tile kernel (double-buffered dQ^T in TMEM).
@@ -1303,7 +1292,6 @@ cudaError_t launch_attn_bwd(const AttnBwdJob& j, cudaStream_t s) {
     p.dV = j.dv.ptr; p.v_sb = j.dv.sb; p.v_sh = j.dv.sh; p.v_ss = j.dv.ss;
     int mode = j.mode;
     if (mode == rgo_attn::MASK_PHILOX && j.threshold >= (uint64_t{1} << 32)) mode = rgo_attn::MASK_NONE;
-    p.debug = bwd_debug_flags();
     cudaError_t e = cudaErrorInvalidValue;
 #define RGO_B(HDV, MODEV, RV) \
     if (j.HD == HDV && mode == MODEV) { e = launch_main<HDV, MODEV, RV>(tq, tk, tv, tdo, p, s); goto launched; }
