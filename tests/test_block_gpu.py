@@ -183,3 +183,37 @@ def test_chunked_pipeline_matches_unchunked(rgo, cuda, mode):
         assert torch.equal(chk.mask[q:], ref.mask[3 * q:])        # slot 1 = chunk 3
     ref.close()
     chk.close()
+
+
+def test_pdl_chain_does_not_change_results(rgo, cuda):
+    """The programmatic-dependent-launch chain (default) against plain stream
+    order (RGO_BLOCK_PDL=0, read once per process: run in a subprocess)."""
+    import hashlib
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import hashlib, sys, torch
+sys.path.insert(0, sys.argv[1])
+import paper_2410_07531_b200 as rgo
+cfg = rgo.WorkloadConfig(batch=2, seq=512, heads=4, head_dim=128, ffn_dim=384, gated=True, keep_prob=0.9,
+                         philox_rounds=10)
+h = hashlib.sha256()
+for mode in ("in_gemm", "no_rng", "serial_fused"):
+    b = rgo.Block(cfg, mode, seed=42)
+    b.step(); b.step()
+    torch.cuda.synchronize()
+    for k in ("x", "qkv", "attn_o", "y1", "h"):
+        h.update(getattr(b, k).view(torch.uint8).cpu().numpy().tobytes())
+    h.update(b.mask.cpu().numpy().tobytes())
+    b.close()
+print(h.hexdigest())
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for pdl in ("1", "0"):
+        env = dict(os.environ, RGO_BLOCK_PDL=pdl)
+        r = subprocess.run([sys.executable, "-c", code, root], env=env, capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out[pdl] = r.stdout.strip().splitlines()[-1]
+    assert out["1"] == out["0"]
