@@ -82,7 +82,7 @@ if os.path.exists(p):
     s = sum(tot.values())
     out = [f"# {RND}: launch list of `bench.py --steps 2 --warmup 3 --no-cpu-baseline` under ncu "
            "(gpu__time_duration.sum)", "",
-           "All kernels of the run: the Llama2-7B and GPT-3 blocks (4 modes x (warm-up + timed) steps), the",
+           "All kernels of the run: the Llama2-7B, GPT-3 and MoE blocks (4 modes x alternating passes x (warm-up + timed) steps), the chunked pipeline, the",
            "stand-alone mask runs, attention fwd+bwd (bits / fused Philox / none) and the SQ sweep.",
            "Serialised, cold-cache times: use the shares.", "", "| kernel | launches | total us | share |",
            "|---|---|---|---|"]
