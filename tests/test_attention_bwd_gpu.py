@@ -128,3 +128,28 @@ def test_bwd_validation(rgo, cuda):
     with pytest.raises(ValueError, match="mask needs"):
         rgo.attn_bwd(q, k, v, o, do, lse, mask_source=rgo.ref_attention.MASK_BITS, keep_prob=0.9,
                      bits=torch.zeros(16, dtype=torch.uint8, device="cuda"))
+
+
+def test_random_shapes_fwd_bwd_vs_oracle(rgo, cuda):
+    """Seeded random sweep: ragged SQ (multiples of 128 and not), both head dims,
+    keep probabilities, round counts, seeds and counter offsets; mask bits from
+    K1 vs inline Philox agree (O, dK, dV bitwise) and match the float64 oracle."""
+    import torch
+    rng = np.random.default_rng(2410)
+    for case in range(12):
+        B, H = int(rng.integers(1, 3)), int(rng.integers(1, 4))
+        S = int(rng.choice([int(rng.integers(1, 700)), 128 * int(rng.integers(1, 5))]))
+        D = int(rng.choice([64, 128]))
+        p = float(rng.choice([0.5, 0.75, 0.9, 0.99]))
+        rounds = int(rng.choice([10, 7, 5]))
+        seed, base = int(rng.integers(0, 2**63)), int(rng.integers(0, 2**40))
+        q, k, v, do = make_inputs(B, H, S, D, 100 + case, qscale=2.0)
+        bits = rgo.generate_mask_device(rgo.MaskLayout(B, H, S, seed, base), rgo.KeepThreshold(p), rounds)
+        ob, dqb, dkb, dvb = run(rgo, q, k, v, do, rgo.ref_attention.MASK_BITS, p, seed, base, rounds, bits)
+        of, dqf, dkf, dvf = run(rgo, q, k, v, do, rgo.ref_attention.MASK_PHILOX, p, seed, base, rounds)
+        ctx = dict(B=B, H=H, S=S, D=D, p=p, rounds=rounds)
+        assert torch.equal(ob, of), ctx
+        assert torch.equal(dkb, dkf) and torch.equal(dvb, dvf), ctx
+        nb = B * H * S * S
+        keep = oracle.unpack_keep(bits[: (nb + 7) // 8].cpu().numpy(), B * H, S)
+        check_vs_oracle(q, k, v, do, ob, dqb, dkb, dvb, keep, p)
