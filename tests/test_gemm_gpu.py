@@ -112,3 +112,22 @@ def test_gemm_validation(rgo, cuda):
     counter = torch.zeros(1, dtype=torch.int64, device="cuda")
     with pytest.raises(ValueError):
         rgo.gemm_with_rng(a, b, c, rgo.mask.desc(lay, rgo.KeepThreshold(0.9), 10), bits, counter, rng_warps=5)
+
+
+def test_random_shapes_vs_torch(rgo, cuda):
+    """Seeded random sweep of ragged M, N (multiple of 32) and K (multiple of 128
+    bytes), FP8 and BF16, against the fp32 product of the same (dequantised) inputs."""
+    import torch
+    rng = np.random.default_rng(7531)
+    for case in range(16):
+        fp8 = bool(case % 2)
+        m = int(rng.integers(1, 1500))
+        n = 32 * int(rng.integers(1, 40))
+        k = (128 if fp8 else 64) * int(rng.integers(1, 12))
+        dt = torch.float8_e4m3fn if fp8 else torch.bfloat16
+        a = make((m, k), torch.float32, 1000 + case, 2.0).to(dt)
+        b = make((n, k), torch.float32, 2000 + case, 2.0).to(dt)
+        alpha = 1.0 / k
+        c = rgo.gemm(a, b, alpha=alpha)
+        ref = (a.float() @ b.float().T) * alpha
+        assert rel(c, ref) < 5e-3, (m, n, k, fp8)
