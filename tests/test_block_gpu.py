@@ -217,3 +217,30 @@ print(h.hexdigest())
         assert r.returncode == 0, r.stderr[-2000:]
         out[pdl] = r.stdout.strip().splitlines()[-1]
     assert out["1"] == out["0"]
+
+
+def test_random_configs_modes_identical(rgo, cuda):
+    """Seeded random block configs: every overlap mode produces the serial-fused
+    block's outputs bitwise, and mechanism A/B masks equal K1's."""
+    import torch
+    rng = np.random.default_rng(11)
+    for case in range(5):
+        cfg = rgo.WorkloadConfig(batch=int(rng.integers(1, 3)), seq=int(rng.choice([256, 384, 512, 640])),
+                                 heads=int(rng.integers(2, 5)), head_dim=128,
+                                 ffn_dim=int(rng.choice([256, 384, 512])), gated=bool(rng.integers(0, 2)),
+                                 keep_prob=float(rng.choice([0.8, 0.9])), philox_rounds=int(rng.choice([7, 10])))
+        seed = int(rng.integers(0, 2**40))
+        outs = {}
+        for mode in ("serial_fused", "streams", "in_gemm"):
+            b = rgo.Block(cfg, mode, seed=seed)
+            b.step()
+            torch.cuda.synchronize()
+            outs[mode] = (snapshot(b), b.mask.clone())
+            b.close()
+        for mode in ("streams", "in_gemm"):
+            for k, v in outs[mode][0].items():
+                assert torch.equal(v.view(torch.uint8), outs["serial_fused"][0][k].view(torch.uint8)), (cfg, mode, k)
+        want = rgo.generate_mask_device(rgo.MaskLayout(cfg.batch, cfg.heads, cfg.seq, seed),
+                                        rgo.KeepThreshold(cfg.keep_prob), cfg.philox_rounds)
+        for mode in ("streams", "in_gemm"):
+            assert torch.equal(outs[mode][1], want[: outs[mode][1].numel()]), (cfg, mode)
