@@ -179,17 +179,18 @@ static GemmJob gemm(const BlockConfig& c, int M, int N, int K, const void* A, co
 // Mechanism B's RNG warps per GEMM CTA when the caller leaves the choice to the
 // block (rng_block = 0): scaled with the mask's Philox work per GEMM flop.  On the
 // power-capped part more RNG warps barely lengthen the GEMM window but shrink the
-// tail drain (scripts/diag/block_phases.py, realistic data, modes interleaved):
-// Llama2-7B (3.2e-4 elements/flop) 8 -> 12 warps: tail 0.41 -> 0.22 ms, step
-// 4.12 -> 3.96 ms (16: 0.12 ms tail, same step); MoE (1.6e-4) and GPT-3 (0.5e-4,
-// Philox-7) leave no tail at 8 and 12/16 only cost GEMM issue slots.
+// tail drain, while with little mask per flop the extra warps only cost GEMM issue
+// slots and power (scripts/diag/block_phases.py, realistic data, PDL chain, modes
+// interleaved): Llama2-7B (3.2e-4 elements/flop) 8 / 12 / 16 warps: step 4.01 /
+// 3.86 / 3.94 ms; MoE (1.6e-4): 4 / 6 / 8 warps 6.87 / 7.03 / 7.05 ms; GPT-3
+// (0.4e-4 at Philox-7): 4 / 6 / 8 warps 3.05 / 3.11 / 3.22 ms.
 static int auto_rng_warps(const BlockConfig& c) {
     const double M = static_cast<double>(c.batch) * c.seq, d = static_cast<double>(c.heads) * c.head_dim;
     const double rows_ffn = c.experts > 0 ? M * c.top_k : M;
     const double flops = 2.0 * M * d * 4.0 * d + 2.0 * rows_ffn * d * c.ffn * ((c.gated ? 2 : 1) + 1);
     const double work = static_cast<double>(c.batch) * c.heads * c.seq * static_cast<double>(c.seq) * c.rounds / 10.0;
     const double r = work / flops;
-    return r <= 2.0e-4 ? 8 : (r <= 3.5e-4 ? 12 : 16);
+    return r <= 1.8e-4 ? 4 : (r <= 2.6e-4 ? 8 : (r <= 3.5e-4 ? 12 : 16));
 }
 
 // Phase-timing events: inside a graph capture they must be external event
