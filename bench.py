@@ -601,6 +601,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true",
                     help="skip the secondary configs (GPT-3 block, attention fwd+bwd, SQ sweep)")
+    ap.add_argument("--watchdog-s", type=float, default=1200.0,
+                    help="exit with an error line if the GPU part has not finished after this many seconds (0 = off)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -624,7 +626,22 @@ def main():
         return
 
     rank, world, _ = dist_setup()
+    # Watchdog: a wedged kernel would otherwise hold the GPU until an outside
+    # timeout; exiting the process tears the context down and frees the GPU.
+    import threading
+
+    def _watchdog():
+        log(f"watchdog: no result after {args.watchdog_s} s, exiting")
+        print(json.dumps({"metric": "llama2_block_ms", "error": f"watchdog: no result after {args.watchdog_s} s"}),
+              flush=True)
+        os._exit(3)
+
+    wd = threading.Timer(args.watchdog_s, _watchdog)
+    wd.daemon = True
+    if args.watchdog_s > 0:
+        wd.start()
     line = bench_block(args, rank, world) if args.workload == "block" else bench_mask_only(args, rank, world)
+    wd.cancel()
     if rank == 0:
         if not args.no_cpu_baseline and world == 1:  # the CPU baseline is an N=1 measurement
             log("CPU baseline (reference, host cores)")
