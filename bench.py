@@ -261,6 +261,29 @@ def block_summary(rgo, wl, res, phases, mask_ms, peaks):
     }
 
 
+def bench_gemms(rgo, wl, world, peaks):
+    import torch
+    f8 = torch.float8_e4m3fn
+    out, tot_flop, tot_ms = {}, 0.0, 0.0
+    for sh in rgo.gemm_shapes(wl):
+        g = torch.Generator(device="cuda").manual_seed(sh.m + sh.n + sh.k)
+        a = ((torch.rand(sh.m, sh.k, device="cuda", generator=g) * 2 - 1) * 1.7).to(f8)
+        b = ((torch.rand(sh.n, sh.k, device="cuda", generator=g) * 2 - 1) * 1.7).to(f8)
+        epi = "swiglu" if sh.name.startswith("FFN1") and wl.gated else ("gelu" if sh.name.startswith("FFN1") else "none")
+        out_dt = torch.bfloat16 if sh.name == "QKV" else f8
+        c = torch.empty(sh.m, sh.n // 2 if epi == "swiglu" else sh.n, dtype=out_dt, device="cuda")
+        ms = event_ms(lambda: rgo.gemm(a, b, c, epilogue=epi, alpha=1.0 / sh.k), 10, world, warm=3)
+        out[sh.name] = {"ms": round(ms, 4), "tflops": round(sh.flops() / ms / 1e9, 1)}
+        tot_flop += sh.flops()
+        tot_ms += ms
+        del a, b, c
+    peak = 2 * peaks["bf16_tflops"]
+    ach = tot_flop / tot_ms / 1e9
+    return {"bound": "tensor", "achieved": round(ach, 1), "peak": round(peak, 1), "unit": "TFLOP/s",
+            "frac": round(ach / peak, 4), "per_gemm": out,
+            "note": "FP8 peak = 2 x measured bf16 (derived); stand-alone, not power-capped by the rest of the step"}
+
+
 def event_ms(fn, reps, world, warm=1):
     import torch
     for _ in range(warm):
@@ -486,6 +509,10 @@ def bench_block(args, rank, world):
         "clocks": clocks, "gpu_launches": launches[best],
     }
     if not args.no_extras:
+        # K2 stand-alone: the block's four FP8 GEMMs (their epilogues as in the block),
+        # each timed alone on unit-variance e4m3 data, against the FP8 peak
+        log("GEMMs stand-alone")
+        line["gemm_roofline"] = bench_gemms(rgo, wl, world, peaks)
         # BASELINE configs[2]: GPT-3 175B block (B1 SQ2048 nH96 d12288, GELU FFN 49152)
         log("GPT-3 block")
         g = rgo.workload_preset("gpt3")
