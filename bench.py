@@ -580,6 +580,23 @@ def bench_block(args, rank, world):
                                  "ratio_R5_R7": round(rr[5] / rr[7], 4), "ratio_R3_R7": round(rr[3] / rr[7], 4),
                                  "paper_ratio_R5_R7": 0.81, "paper_ratio_R3_R7": 0.67,
                                  "config": "K1 stand-alone, Llama2-7B mask (2^31 elements), keep 0.9"}
+        # the Llama2-7B block with reduced-round Philox: fused baseline vs
+        # mechanism B at the same round count
+        log("block at reduced rounds")
+        br = {}
+        for R in (3, 5, 7):
+            wr = rgo.workload_preset("llama2_7b")
+            wr.philox_rounds = R
+            rblocks, rres, _, _, _ = run_block_modes(rgo, wr, rank, world, args, ["serial_fused", "in_gemm", "no_rng"])
+            for blk in rblocks.values():
+                blk.close()
+            del rblocks
+            torch.cuda.empty_cache()
+            br[f"R{R}"] = {"modes_ms": {m: round(v, 4) for m, v in rres.items()},
+                           "speedup_vs_fused": round(rres["serial_fused"] / rres["in_gemm"], 4)}
+        br["R10"] = {"modes_ms": {m: line["modes_ms"][m] for m in ("serial_fused", "in_gemm", "no_rng")},
+                     "speedup_vs_fused": round(line["modes_ms"]["serial_fused"] / line["modes_ms"]["in_gemm"], 4)}
+        line["block_rounds"] = br
     return line
 
 

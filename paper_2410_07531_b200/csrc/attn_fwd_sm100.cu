@@ -541,6 +541,12 @@ cudaError_t launch_attn_fwd(const AttnJob& j, cudaStream_t s) {
         } else if (j.rounds == 7) {
             RGO_A(128, MASK_PHILOX, 7)
             RGO_A(64, MASK_PHILOX, 7)
+        } else if (j.rounds == 5) {  // reduced-round baselines
+            RGO_A(128, MASK_PHILOX, 5)
+            RGO_A(64, MASK_PHILOX, 5)
+        } else if (j.rounds == 3) {
+            RGO_A(128, MASK_PHILOX, 3)
+            RGO_A(64, MASK_PHILOX, 3)
         } else {
             RGO_A(128, MASK_PHILOX, 0)
             RGO_A(64, MASK_PHILOX, 0)

@@ -92,6 +92,10 @@ __device__ __forceinline__ void rng_queue_drain(const RngQueue& q, const volatil
         rng_drain_r<10>(q, stop, stop_at);
     else if (q.rounds == 7)
         rng_drain_r<7>(q, stop, stop_at);
+    else if (q.rounds == 5)
+        rng_drain_r<5>(q, stop, stop_at);
+    else if (q.rounds == 3)
+        rng_drain_r<3>(q, stop, stop_at);
     // other round counts are served by the tail kernel (rng_queue_kernel)
 }
 

@@ -244,3 +244,23 @@ def test_random_configs_modes_identical(rgo, cuda):
                                         rgo.KeepThreshold(cfg.keep_prob), cfg.philox_rounds)
         for mode in ("streams", "in_gemm"):
             assert torch.equal(outs[mode][1], want[: outs[mode][1].numel()]), (cfg, mode)
+
+
+@pytest.mark.parametrize("rounds", [5, 3])
+def test_reduced_round_in_gemm_block(rgo, cuda, rounds):
+    """Philox-5/-3: the in-GEMM drains (and the matching inline-Philox baseline)
+    keep the modes bitwise equal and the mask equal to K1's."""
+    import torch
+    cfg = rgo.WorkloadConfig(batch=2, seq=512, heads=4, head_dim=128, ffn_dim=384, gated=True, keep_prob=0.9,
+                             philox_rounds=rounds)
+    outs = {}
+    for mode in ("serial_fused", "in_gemm"):
+        b = rgo.Block(cfg, mode, seed=9)
+        b.step()
+        torch.cuda.synchronize()
+        outs[mode] = (snapshot(b), b.mask.clone())
+        b.close()
+    for k, v in outs["in_gemm"][0].items():
+        assert torch.equal(v.view(torch.uint8), outs["serial_fused"][0][k].view(torch.uint8)), k
+    want = rgo.generate_mask_device(rgo.MaskLayout(2, 4, 512, 9), rgo.KeepThreshold(0.9), rounds)
+    assert torch.equal(outs["in_gemm"][1], want[: outs["in_gemm"][1].numel()])
