@@ -184,6 +184,111 @@ def cpu_reference_block(cfg, target_s=10.0, kind="reference"):
             "mask_s": t_mask, "attention_s": t_att, "sample_wall_s": t_att_wall}
 
 
+def host_cpu_info():
+    """lscpu model name + the thread count the CPU arms use (= std::thread::
+    hardware_concurrency(), mask.hpp:163)."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except Exception:  # noqa: BLE001
+        pass
+    if model is None:
+        try:
+            with open("/proc/cpuinfo") as f:
+                model = next((ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name")), None)
+        except OSError:
+            pass
+    return {"model": model, "hardware_concurrency": os.cpu_count() or 1}
+
+
+def cpu_baseline_suite(rounds=10, kind="reference"):
+    """BASELINE.md section 4 on this host's cores: the reference's generate_mask
+    (mask.hpp:142-179, workers = hardware_concurrency) at the O, L, G and S
+    shapes (S: a bounded per-slice sample of B1 nH32 at each SQ, extrapolated
+    to 32 slices, as the 2^36-bit guard forces for the larger layouts), and
+    attention_forward / _decoupled / _fused (ref_attention.hpp:108-146) at the
+    O config both single-threaded (as the reference runs it) and one slice per
+    core (base_offset = s*SQ^2/4, bitwise that slice of the full run)."""
+    import numpy as np
+    oracle = _oracle()
+    use_ref = kind == "reference" and oracle.ref_available()
+    R = oracle.ref() if use_ref else None
+    O = oracle.lib()
+    info = host_cpu_info()
+    cores = info["hardware_concurrency"]
+    out = {"kind": "reference" if use_ref else "port", "host": info, "rounds": rounds}
+
+    def mask_s(B, H, S, workers, base=0):
+        n = B * H * S * S
+        buf = np.zeros((n + 7) // 8, np.uint8)
+        t0 = time.perf_counter()
+        if use_ref:
+            assert R.ref_generate_mask(B, H, S, 42, base, 0.9, rounds, workers, buf, buf.size) == 0
+        else:
+            thr, _ = oracle.keep_threshold(0.9)
+            O.oracle_generate_mask(n, 42, base, thr, rounds, workers, buf, buf.size)
+        return time.perf_counter() - t0, buf
+
+    masks = {}
+    for name, (B, H, S) in {"O": (1, 8, 512), "L": (4, 32, 4096), "G": (1, 96, 2048)}.items():
+        t, buf = mask_s(B, H, S, cores)
+        n = B * H * S * S
+        masks[name] = {"layout": f"B{B} nH{H} SQ{S}", "s": round(t, 4), "gbit_s": round(n / t / 1e9, 3),
+                       "threads": cores}
+        if name == "O":
+            t1, _ = mask_s(B, H, S, 1)
+            masks["O"]["s_1thread"] = round(t1, 4)
+    sweep = []
+    for S in (1024, 2048, 4096, 8192, 16384, 32768):
+        n_sl = max(1, min(32, (1 << 31) // (S * S)))
+        t, _ = mask_s(1, n_sl, S, cores)
+        sweep.append({"seq": S, "slices_timed": n_sl, "s_32_slices": round(t * 32 / n_sl, 3),
+                      "gbit_s": round(n_sl * S * S / t / 1e9, 3)})
+    masks["S_sweep_B1_nH32"] = sweep
+    out["masks"] = masks
+    # attention at config O (B1 nH8 SQ512 dH64, keep 0.9)
+    sl, S, D = 8, 512, 64
+    q, k, v = oracle.random_attention_input(sl, S, D, 42 ^ 0xA77E)
+    _, bits = mask_s(1, sl, S, cores)
+
+    def attn(mode, s0, s1):
+        """mode 0 plain, 1 fused, 2 decoupled over slices [s0, s1)."""
+        n = (s1 - s0) * S * D
+        qs, ks, vs = (x[s0 * S * D: s1 * S * D].copy() for x in (q, k, v))
+        o = np.zeros(n, np.float32)
+        base = s0 * S * S // 4
+        if use_ref:
+            if mode == 2:
+                mb = bits[s0 * S * S // 8: s1 * S * S // 8].copy()
+                rc = R.ref_attention_decoupled(s1 - s0, S, D, qs, ks, vs, mb, mb.size, 0.9, rounds, o)
+            else:
+                rc = R.ref_attention(s1 - s0, S, D, qs, ks, vs, mode, 42, base, 0.9, rounds, o)
+        else:
+            thr, pf = oracle.keep_threshold(0.9)
+            mb = bits[s0 * S * S // 8:].copy() if mode == 2 else None
+            rc = O.oracle_attention(s1 - s0, S, D, qs, ks, vs, mode, 42, base, thr, pf, rounds,
+                                    None if mb is None else mb.ctypes.data, 0, s1 - s0, o)
+        assert rc == 0
+        return o
+
+    att = {"config": "O: B1 nH8 SQ512 dH64 keep 0.9"}
+    for mode, name in ((0, "plain"), (2, "decoupled"), (1, "fused")):
+        t0 = time.perf_counter()
+        attn(mode, 0, sl)
+        att[f"{name}_s_1thread"] = round(time.perf_counter() - t0, 4)
+        t0 = time.perf_counter()
+        with cf.ThreadPoolExecutor(min(cores, sl)) as ex:
+            list(ex.map(lambda s: attn(mode, s, s + 1), range(sl)))
+        att[f"{name}_s_slice_per_core"] = round(time.perf_counter() - t0, 4)
+    att["threads_slice_per_core"] = min(cores, sl)
+    out["attention_O"] = att
+    return out
+
+
 # --------------------------------------------------------------------- GPU side
 def time_steps(fn, steps, world, stream):
     import torch
@@ -243,6 +348,48 @@ def run_block_modes(rgo, wl, rank, world, args, modes, chunks=1, passes=1):
     return blocks, res, samples, phases, launches
 
 
+def golden_mask_fnv(name, rounds):
+    """The reference's FNV-1a-64 of the full mask (tests/golden/golden.json, recorded
+    from the reference compiled in place, oracle/make_golden.py), or None."""
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "golden.json")) as f:
+            big = json.load(f)["big_masks"]
+    except (OSError, ValueError, KeyError):
+        return None
+    for m in big:
+        if m["name"] == name and m["rounds"] == rounds and m["base_offset"] == 0 and m["seed"] == 42:
+            return m["fnv"]
+    return None
+
+
+def block_parity(rgo, blocks, golden_name, rounds, rank):
+    """Self-check of the timed run, after the timed region: the in-GEMM (and
+    streams) mask left by the last timed step is copied back and hashed
+    (FNV-1a-64 through the C ABI) against the reference's hash of the same
+    layout; every mode's attention output must equal the serial-fused
+    (Philox-inline) baseline's bitwise.  Rank r > 0 checks its own replica's
+    disjoint counter range against rank 0's hash only when r == 0."""
+    import torch
+    torch.cuda.synchronize()
+    out = {"golden": golden_name, "rounds": rounds}
+    ok = True
+    want = golden_mask_fnv(golden_name, rounds) if rank == 0 else None
+    for m in ("in_gemm", "streams"):
+        if m not in blocks:
+            continue
+        h = f"{rgo.mask.fnv1a64(blocks[m].mask.cpu()):016x}"
+        out[f"mask_fnv_{m}"] = h
+        if want is not None:
+            ok &= h == want
+    out["golden_fnv"] = want
+    base = blocks["serial_fused"].attn_o.view(torch.uint8)
+    eq = {m: bool(torch.equal(b.attn_o.view(torch.uint8), base)) for m, b in blocks.items() if m != "serial_fused"}
+    out["attn_o_bitwise_equal_to_fused"] = eq
+    ok &= all(eq.values())
+    out["ok"] = bool(ok)
+    return out
+
+
 def block_summary(rgo, wl, res, phases, mask_ms, peaks):
     gemm_flops = sum(g.flops() for g in rgo.gemm_shapes(wl))
     attn_flops = rgo.attention_work(wl)[0]
@@ -259,6 +406,107 @@ def block_summary(rgo, wl, res, phases, mask_ms, peaks):
         "mask_ms": round(mask_ms, 4),
         "block_roofline": {"ms": round(roof_ms, 4), "frac": round(roof_ms / value, 4)},
     }
+
+
+def bench_e2e(rgo, wl, b, mode, args, world):
+    import torch
+    stream = torch.cuda.current_stream()
+    b2 = rgo.Block(wl, mode, seed=42, base_offset=b.desc.base_offset, weights=b.weights,
+                   rng_launch=(tuple(args.rng_launch) if mode == "streams" else (0, args.rng_warps, 0)))
+    pair = (b, b2)
+    host_in = [t.cpu().pin_memory() for t in (b.attn_in, (b.attn_in.float() * -1.0).bfloat16())]
+    host_out = [torch.empty_like(b.attn_o, device="cpu").pin_memory() for _ in range(2)]
+    h2d, d2h = torch.cuda.Stream(), torch.cuda.Stream()
+    ev_in = [torch.cuda.Event() for _ in range(2)]
+    ev_step = [torch.cuda.Event() for _ in range(2)]
+    ev_done = [torch.cuda.Event() for _ in range(2)]   # replica's previous result is in host memory
+    state = {"k": 0}
+
+    def stage_input(slot, k):
+        with torch.cuda.stream(h2d):
+            h2d.wait_event(ev_done[slot])
+            pair[slot].attn_in.copy_(host_in[k % 2], non_blocking=True)
+            ev_in[slot].record(h2d)
+
+    for slot in range(2):
+        ev_done[slot].record(stream)
+    stage_input(0, 0)
+
+    def e2e_step():
+        k = state["k"]
+        cur, nxt = k % 2, (k + 1) % 2
+        stage_input(nxt, k + 1)                 # H2D of step k+1's input, overlapped
+        stream.wait_event(ev_in[cur])
+        n = pair[cur].step()
+        ev_step[cur].record(stream)
+        with torch.cuda.stream(d2h):            # D2H of the whole result, overlapped
+            d2h.wait_event(ev_step[cur])
+            host_out[cur].copy_(pair[cur].attn_o, non_blocking=True)
+            ev_done[cur].record(d2h)
+        state["k"] = k + 1
+        return n
+
+    for _ in range(max(10, args.warmup)):  # back to the steady power state the modes ran in
+        e2e_step()
+    torch.cuda.synchronize()
+    barrier(world)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    for slot in range(2):                   # the timed region ends with the last D2H
+        stream.wait_event(ev_done[slot])
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps, world)
+    # the last result really is the step's output
+    last = (state["k"] - 1) % 2
+    assert torch.equal(host_out[last].view(torch.uint8), pair[last].attn_o.cpu().view(torch.uint8))
+    b2.close()
+    h2d_bytes = int(host_in[0].numel() * host_in[0].element_size())
+    d2h_bytes = int(host_out[0].numel() * host_out[0].element_size())
+    return ms, h2d_bytes, d2h_bytes
+
+
+def bench_dropin_O(rgo, reps=20):
+    """The drop-in surface end to end at config O (B1 nH8 SQ512 dH64, keep 0.9,
+    Philox-10): generate_mask (mask.hpp:142-179) then attention_dropout_decoupled
+    (ref_attention.hpp:129-146) on HOST float arrays through the C ABI the
+    include/rgo/*.hpp drop-in calls (rgo_generate_mask_host + rgo_attention_host:
+    H2D, K1 / K5, D2H inside each call).  Wall clock per pair of calls, median."""
+    import ctypes as C
+    import numpy as np
+    L_ = rgo._lib
+    lib = L_.lib()
+    sl, S, D = 8, 512, 64
+    n = sl * S * D
+    q, k, v = (np.empty(n, np.float32) for _ in range(3))
+    L_.check(lib.rgo_random_attention_input_host(sl, S, D, 42 ^ 0xA77E, q.ctypes.data, k.ctypes.data, v.ctypes.data))
+    thr = C.c_uint64()
+    L_.check(lib.rgo_keep_threshold(0.9, C.byref(thr), None))
+    md = L_.mask_desc(1, sl, S, 10, 42, 0, thr.value)
+    bits = np.empty(sl * S * S // 8, np.uint8)
+    o = np.empty(n, np.float32)
+    ad = L_.attn_host_desc(sl, S, D, 1, 0.9, 0, 0, 10, 0)  # RGO_MASK_BITS
+
+    def once():
+        L_.check(lib.rgo_generate_mask_host(md, bits.ctypes.data, bits.size, 1))
+        L_.check(lib.rgo_attention_host(C.byref(ad), q.ctypes.data, k.ctypes.data, v.ctypes.data, bits.ctypes.data,
+                                        bits.size, o.ctypes.data))
+    for _ in range(3):
+        once()
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        once()
+        ts.append(time.perf_counter() - t0)
+    ts.sort()
+    return {"value_ms": round(ts[len(ts) // 2] * 1e3, 3), "unit": "ms per generate_mask + attention_dropout_decoupled",
+            "h2d_bytes": int(3 * n * 4 + bits.size), "d2h_bytes": int(bits.size + n * 4),
+            "config": "O: B1 nH8 SQ512 dH64 keep 0.9 Philox-10, host float arrays through the C ABI "
+                      "(rgo_generate_mask_host + rgo_attention_host), median of %d" % reps,
+            "mask_fnv": f"{rgo.mask.fnv1a64(bits):016x}"}
 
 
 def bench_gemms(rgo, wl, world, peaks):
@@ -408,53 +656,17 @@ def bench_block(args, rank, world):
     mask_ms, _ = bench_mask_kernel(rgo, cfg, rank, max(5, args.steps // 2), 3)
     mask_ms = max_over_ranks(mask_ms, world)
     best, value, summ = block_summary(rgo, wl, res, phases, mask_ms, peaks)
+    parity = block_parity(rgo, blocks, "L", cfg["rounds"], rank)
     # ----- e2e through the public API with host buffers.  A step's input is the
     # previous block's attention output (`attn_in`, bf16 [M, d], 128 MiB, read by the
-    # step's first kernel); every timed step copies a fresh one from pinned host memory and
-    # reads back a row block of its result.  Two block replicas alternate so the
-    # next step's 128 MiB H2D (copy stream) overlaps the current step, as a
-    # serving loop would do.
+    # step's first kernel) and its result is this block's attention output (`attn_o`,
+    # bf16 [M, d], 128 MiB).  Every timed step copies a fresh input from pinned host
+    # memory (H2D copy stream) and copies its WHOLE result back into pinned host memory
+    # (D2H copy stream).  Two block replicas alternate so step k+1's H2D and step k's
+    # D2H overlap the compute of the neighbouring steps, as a serving loop would; the
+    # timed region ends when the last step's result has landed in host memory.
     log("e2e")
-    b = blocks[best]
-    stream = torch.cuda.current_stream()
-    b2 = rgo.Block(wl, best, seed=42, base_offset=b.desc.base_offset, weights=b.weights,
-                   rng_launch=(tuple(args.rng_launch) if best == "streams" else (0, args.rng_warps, 0)))
-    pair = (b, b2)
-    host_in = [t.cpu().pin_memory() for t in (b.attn_in, (b.attn_in.float() * -1.0).bfloat16())]
-    out_host = torch.empty(4096, dtype=torch.bfloat16).pin_memory()
-    copy_stream = torch.cuda.Stream()
-    ev_in = [torch.cuda.Event() for _ in range(2)]
-    ev_done = [torch.cuda.Event() for _ in range(2)]
-    state = {"k": 0}
-
-    def stage_input(slot, k):
-        with torch.cuda.stream(copy_stream):
-            copy_stream.wait_event(ev_done[slot])
-            pair[slot].attn_in.copy_(host_in[k % 2], non_blocking=True)
-            ev_in[slot].record(copy_stream)
-
-    for slot in range(2):
-        ev_done[slot].record(stream)
-    stage_input(0, 0)
-
-    def e2e_step():
-        k = state["k"]
-        cur, nxt = k % 2, (k + 1) % 2
-        stage_input(nxt, k + 1)                 # H2D of step k+1's input, overlapped
-        stream.wait_event(ev_in[cur])
-        n = pair[cur].step()
-        out_host.copy_(pair[cur].attn_o.view(-1)[:4096], non_blocking=True)  # D2H of the result
-        ev_done[cur].record(stream)
-        state["k"] = k + 1
-        return n
-
-    for _ in range(max(10, args.warmup)):  # back to the steady power state the modes ran in
-        e2e_step()
-    e2e_ms, _ = time_steps(e2e_step, args.steps, world, stream)
-    torch.cuda.synchronize()
-    e2e_ms = max_over_ranks(e2e_ms, world)
-    b2.close()
-    h2d_bytes = int(host_in[0].numel() * host_in[0].element_size())
+    e2e_ms, h2d_bytes, d2h_bytes = bench_e2e(rgo, wl, blocks[best], best, args, world)
     for blk in blocks.values():
         blk.close()
     del blocks
@@ -502,10 +714,13 @@ def bench_block(args, rank, world):
                      "traffic": profiled_traffic("attn_fwd_bits"),
                      "algorithmic": f"4*B*nH*SQ^2*dH = {attn_flops:.4e} flop per launch (workload.hpp:59-64)"},
         "e2e": {"value": round(e2e_ms, 4), "unit": "ms", "h2d_bytes_per_step": h2d_bytes,
-                "d2h_bytes_per_step": int(out_host.numel() * 2),
-                "how": "public API (Block.step), step input = previous attention output copied from pinned "
-                       "host memory every step (overlapped with the previous step on a copy stream, two "
-                       "replicas alternating), result row block read back every step"},
+                "d2h_bytes_per_step": d2h_bytes,
+                "how": "public API (Block.step), step input (previous attention output, bf16 [M, d]) copied "
+                       "from pinned host memory every step on an H2D stream, the step's whole result "
+                       "(attention output, bf16 [M, d]) copied back to pinned host memory every step on a "
+                       "D2H stream; two replicas alternate so copies overlap neighbouring steps; the timed "
+                       "region ends when the last result is in host memory"},
+        "parity": parity,
         "clocks": clocks, "gpu_launches": launches[best],
     }
     if not args.no_extras:
@@ -518,6 +733,7 @@ def bench_block(args, rank, world):
         g = rgo.workload_preset("gpt3")
         g.philox_rounds = args.rounds
         gblocks, gres, _, gph, _ = run_block_modes(rgo, g, rank, world, args, modes, passes=2)
+        gparity = block_parity(rgo, gblocks, "G", args.rounds, rank)
         for blk in gblocks.values():
             blk.close()
         del gblocks
@@ -527,7 +743,8 @@ def bench_block(args, rank, world):
         _, gval, gsum = block_summary(rgo, g, gres, gph, max_over_ranks(gmask, world), peaks)
         line["gpt3_block"] = dict({"value_ms": round(gval, 4),
                                    "config": "GPT-3 175B block FP8: B1 SQ2048 nH96 dH128 d12288, GELU FFN 49152, "
-                                             "keep 0.9, Philox-10"}, **gsum)
+                                             "keep 0.9, Philox-10", "parity": gparity}, **gsum)
+        line["parity"]["ok"] = bool(line["parity"]["ok"] and gparity["ok"])
         # BASELINE configs[3]: MoE block (Mixtral-8x7B-like): 8 experts top-2 SwiGLU FFN 14336
         log("MoE block")
         mo = rgo.workload_preset("moe")
@@ -693,6 +910,9 @@ def main():
             line["cpu_baseline"] = {k: (round(cb[k], 1) if k == "value" else cb[k])
                                     for k in ("value", "unit", "cores", "kind", "sample")}
         print(json.dumps(line))
+        if "parity" in line and not line["parity"]["ok"]:
+            log(f"PARITY FAILURE: {line['parity']}")
+            sys.exit(1)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

@@ -97,6 +97,13 @@ int rgo_mask_generate_ex(const rgo_mask_desc* d, uint8_t* d_bits, uint64_t bytes
  * depend on it, mask.hpp:139-141) and copies the bits to h_bits. */
 int rgo_generate_mask_host(const rgo_mask_desc* d, uint8_t* h_bits, uint64_t bytes,
                            uint32_t devices);
+/* As rgo_generate_mask_host, split into `shards` (>= devices; 0 = one per
+ * device) byte-aligned shards, each generated from its own counter offset and
+ * copied into place; shard r runs on device (current + r % devices).  The
+ * bytes never depend on devices or shards (mask.hpp:139-141); shards > devices
+ * exercises the multi-device slicing on one GPU. */
+int rgo_generate_mask_host_ex(const rgo_mask_desc* d, uint8_t* h_bits, uint64_t bytes,
+                              uint32_t devices, uint32_t shards);
 
 /* ------------------------------------------------------- synthetic inputs --
  * random_attention_input's generator (ref_attention.hpp:186-202) on device:
@@ -243,6 +250,11 @@ int rgo_mask_save(const char* path, const rgo_mask_desc* d, float keep_prob, con
                   uint64_t bytes);
 int rgo_mask_load(const char* path, rgo_mask_desc* d, float* keep_prob, uint8_t* h_bits,
                   uint64_t capacity, uint64_t* bytes);
+
+/* FNV-1a-64 of n host bytes (offset 0xcbf29ce484222325, prime 0x100000001b3):
+ * the checksum the golden mask fixtures are recorded with; lets a caller
+ * self-check a device mask it copied back (bench.py's parity block). */
+uint64_t rgo_fnv1a64(const uint8_t* h_data, uint64_t n);
 
 /* ----------------------------------------------------------------- block --
  * Transformer-block step (the paper's timeline, schedule.hpp:111-136): the

@@ -77,6 +77,8 @@ def ref():
         d.ref_random_attention_input.restype = None
         d.ref_attention.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, _f32p, _f32p, _f32p, C.c_int,
                                     C.c_uint64, C.c_uint64, C.c_double, C.c_int, _f32p]
+        d.ref_attention_decoupled.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, _f32p, _f32p, _f32p, _u8p,
+                                              C.c_uint64, C.c_double, C.c_int, _f32p]
         d.ref_gemm_shapes.argtypes = [C.c_uint32] * 5 + [np.ctypeslib.ndpointer(np.uint64, flags="C")]
         d.ref_philox_test_vectors.argtypes = [C.c_uint64, C.c_int, C.c_int, _u32p, _u32p, _i32p, _u32p]
         d.ref_philox_test_vectors.restype = None
@@ -169,17 +171,17 @@ def attention_backward(q, k, v, do, slices, seq, head_dim, keep=None, p=1.0):
     q, k, v, do = (np.asarray(x, np.float64).reshape(sh) for x in (q, k, v, do))
     scale = float(np.float32(1.0) / np.sqrt(np.float32(head_dim)))
     pf = float(np.float32(p))
-    s = scale * np.einsum("sid,sjd->sij", q, k)
+    s = scale * (q @ k.transpose(0, 2, 1))
     s -= s.max(axis=-1, keepdims=True)
     e = np.exp(s)
     P = e / e.sum(axis=-1, keepdims=True)
     km = np.ones_like(P) if keep is None else keep.astype(np.float64)
     W = km * P / pf
-    o = np.einsum("sij,sjd->sid", W, v)
-    dv = np.einsum("sij,sid->sjd", W, do)
-    dP = km * np.einsum("sid,sjd->sij", do, v) / pf
+    o = W @ v
+    dv = W.transpose(0, 2, 1) @ do
+    dP = km * (do @ v.transpose(0, 2, 1)) / pf
     D = (P * dP).sum(axis=-1, keepdims=True)
     dS = P * (dP - D)
-    dq = scale * np.einsum("sij,sjd->sid", dS, k)
-    dk = scale * np.einsum("sij,sid->sjd", dS, q)
+    dq = scale * (dS @ k)
+    dk = scale * (dS.transpose(0, 2, 1) @ q)
     return o, dq, dk, dv

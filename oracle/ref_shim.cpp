@@ -100,6 +100,27 @@ int ref_attention(uint32_t slices, uint32_t seq, uint32_t head_dim, const float*
     }
 }
 
+// attention_dropout_decoupled (ref_attention.hpp:129-146) with the caller's packed
+// mask bits (layout batch 1, heads = slices): times the attention alone, without
+// the generate_mask that ref_attention's mode 2 runs first.
+int ref_attention_decoupled(uint32_t slices, uint32_t seq, uint32_t head_dim, const float* q,
+                            const float* k, const float* v, const uint8_t* bits, uint64_t nbytes,
+                            double p, int rounds, float* o) {
+    try {
+        const rgo::AttentionInput in = make_input(slices, seq, head_dim, q, k, v);
+        rgo::DropoutMask m;
+        m.layout.batch = 1; m.layout.heads = slices; m.layout.seq = seq;
+        m.keep_prob = static_cast<float>(p);
+        m.rounds = static_cast<uint32_t>(rounds);
+        m.bits.assign(bits, bits + nbytes);
+        const rgo::AttentionOutput out = rgo::attention_dropout_decoupled(in, m, p);
+        std::memcpy(o, out.o.data(), out.o.size() * 4);
+        return 0;
+    } catch (const std::invalid_argument&) {
+        return -1;
+    }
+}
+
 // gemm_shapes (workload.hpp:44-52): fills m,n,k for QKV, Proj, FFN1, FFN2.
 int ref_gemm_shapes(uint32_t batch, uint32_t seq, uint32_t heads, uint32_t head_dim,
                     uint32_t ffn_factor, uint64_t mnk[12]) {

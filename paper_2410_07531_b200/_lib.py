@@ -70,6 +70,14 @@ class attn_desc(C.Structure):
     ]
 
 
+class attn_host_desc(C.Structure):
+    _fields_ = [
+        ("slices", C.c_uint32), ("seq", C.c_uint32), ("head_dim", C.c_uint32), ("mask_source", C.c_int32),
+        ("keep_prob", C.c_double), ("seed", C.c_uint64), ("base_offset", C.c_uint64), ("rounds", C.c_uint32),
+        ("reserved", C.c_uint32),
+    ]
+
+
 class block_desc(C.Structure):
     _fields_ = [
         ("batch", C.c_uint32), ("seq", C.c_uint32), ("heads", C.c_uint32), ("head_dim", C.c_uint32),
@@ -109,6 +117,11 @@ SIGNATURES = {
         C.c_int,
         [C.POINTER(mask_desc), C.c_void_p, C.c_uint64, C.c_uint32],
     ),
+    "rgo_generate_mask_host_ex": (
+        C.c_int,
+        [C.POINTER(mask_desc), C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32],
+    ),
+    "rgo_fnv1a64": (C.c_uint64, [C.c_void_p, C.c_uint64]),
     "rgo_mask_queue_drain": (
         C.c_int,
         [C.POINTER(mask_desc), C.c_void_p, C.c_uint64, C.c_void_p, C.POINTER(launch), C.c_void_p],

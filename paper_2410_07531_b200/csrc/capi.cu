@@ -161,6 +161,11 @@ int rgo_mask_generate(const rgo_mask_desc* d, uint8_t* d_bits, uint64_t bytes,
 
 int rgo_generate_mask_host(const rgo_mask_desc* d, uint8_t* h_bits, uint64_t bytes,
                            uint32_t devices) {
+    return rgo_generate_mask_host_ex(d, h_bits, bytes, devices, 0);
+}
+
+int rgo_generate_mask_host_ex(const rgo_mask_desc* d, uint8_t* h_bits, uint64_t bytes,
+                              uint32_t devices, uint32_t shards) {
     if (int e = validate_mask(d, "generate_mask")) return e;
     const uint64_t n = elem_count(d);
     if (n > kMaxBits)  // mask.hpp:148-155
@@ -174,21 +179,25 @@ int rgo_generate_mask_host(const rgo_mask_desc* d, uint8_t* h_bits, uint64_t byt
     if (int e = require_device()) return e;
     int ndev = rgo_device_count();
     if (devices == 0 || devices > static_cast<uint32_t>(ndev)) devices = static_cast<uint32_t>(ndev);
+    if (shards < devices) shards = devices;
+    // Device of shard r: the caller's current device first, then the following
+    // ordinals (wrapping), round-robin over `devices` -- a single-device call
+    // runs on the current device, never silently on device 0.
+    int prev = 0;
+    cudaGetDevice(&prev);
     // Shard on 16-byte (128-element) boundaries: shard r covers elements
     // [e0, e1) and is the mask of the same layout with base_offset + e0/4,
     // so the shards concatenate to the single-device bytes (mask.hpp:139-141).
     const uint64_t nvec = (nbytes + 15) / 16;
-    const uint64_t per = (nvec + devices - 1) / devices;
-    int prev = 0;
-    cudaGetDevice(&prev);
-    std::vector<int> status(devices, RGO_OK);
-    std::vector<std::string> msgs(devices);
+    const uint64_t per = (nvec + shards - 1) / shards;
+    std::vector<int> status(shards, RGO_OK);
+    std::vector<std::string> msgs(shards);
     auto work = [&](uint32_t r) {
         const uint64_t v0 = r * per, v1 = std::min(nvec, v0 + per);
         if (v0 >= v1) return;
         const uint64_t e0 = v0 * 128, e1 = std::min(n, v1 * 128);
         const uint64_t b0 = v0 * 16, b1 = std::min(nbytes, v1 * 16);
-        cudaSetDevice(static_cast<int>(r));
+        cudaSetDevice((prev + static_cast<int>(r % devices)) % ndev);
         uint8_t* dbuf = nullptr;
         cudaError_t ce = cudaMalloc(&dbuf, (b1 - b0 + 15) & ~uint64_t{15});
         if (ce != cudaSuccess) {
@@ -206,17 +215,18 @@ int rgo_generate_mask_host(const rgo_mask_desc* d, uint8_t* h_bits, uint64_t byt
             msgs[r] = cudaGetErrorString(ce);
         }
     };
-    if (devices == 1) {
+    if (shards == 1) {
         work(0);
     } else {
         std::vector<std::thread> pool;
-        for (uint32_t r = 0; r < devices; ++r) pool.emplace_back(work, r);
+        for (uint32_t r = 0; r < shards; ++r) pool.emplace_back(work, r);
         for (auto& t : pool) t.join();
     }
     cudaSetDevice(prev);
-    for (uint32_t r = 0; r < devices; ++r)
+    for (uint32_t r = 0; r < shards; ++r)
         if (status[r] != RGO_OK)
-            return fail(status[r], "generate_mask (device %u): %s", r, msgs[r].c_str());
+            return fail(status[r], "generate_mask (shard %u, device %d): %s", r,
+                        (prev + static_cast<int>(r % devices)) % ndev, msgs[r].c_str());
     return RGO_OK;
 }
 
@@ -452,6 +462,22 @@ int rgo_block_create(const rgo_block_desc* d, const rgo_block_buffers* b, int32_
     if (d->head_dim != 64 && d->head_dim != 128) return fail(RGO_EINVAL, "rgo_block_create: head_dim 64/128");
     if (!(d->keep_prob > 0.0 && d->keep_prob < 1.0)) return fail(RGO_EINVAL, "rgo_block_create: keep_prob in (0,1)");
     if (d->rounds < 1 || d->rounds > 16) return fail(RGO_EINVAL, "rgo_block_create: rounds must be in [1,16]");
+    {
+        // keep_prob is used as a float (mask.hpp:59): a double in (0,1) can still round
+        // to a threshold of 0 (keep nothing) or 2^32 (keep all), which the in-GEMM
+        // queue's 32-bit compare cannot express -- the modes would silently disagree
+        uint64_t thr0 = 0;
+        rgo_keep_threshold(d->keep_prob, &thr0, nullptr);
+        if (thr0 == 0 || thr0 >= (uint64_t{1} << 32))
+            return fail(RGO_EINVAL, "rgo_block_create: keep_prob %.17g rounds (as float) to a threshold of %llu; "
+                                    "needs 0 < threshold < 2^32", d->keep_prob, static_cast<unsigned long long>(thr0));
+    }
+    if (mode == RGO_OVERLAP_IN_GEMM) {
+        const uint32_t rw = d->rng_launch.block;
+        if (rw != 0 && rw != 4 && rw != 6 && rw != 8 && rw != 12 && rw != 16)
+            return fail(RGO_EINVAL, "rgo_block_create: IN_GEMM rng_launch.block = RNG warps per GEMM CTA must be "
+                                    "0, 4, 6, 8, 12 or 16 (got %u)", rw);
+    }
     const uint64_t dm = static_cast<uint64_t>(d->heads) * d->head_dim;
     if (dm % 256 || d->ffn % 128 || (static_cast<uint64_t>(d->batch) * d->seq) % 128 || d->seq % 128)
         return fail(RGO_EINVAL, "rgo_block_create: needs d %% 256, ffn %% 128, seq %% 128 == 0");

@@ -34,6 +34,7 @@ RGO_GEMM_EXTERN(true, EPI_NONE, OUT_E4M3)
 RGO_GEMM_EXTERN(true, EPI_SWIGLU, OUT_E4M3)
 RGO_GEMM_EXTERN(true, EPI_SWIGLU, OUT_BF16)
 RGO_GEMM_EXTERN(true, EPI_GELU, OUT_E4M3)
+RGO_GEMM_EXTERN(true, EPI_GELU, OUT_BF16)
 RGO_GEMM_EXTERN(false, EPI_NONE, OUT_BF16)
 RGO_GEMM_EXTERN(false, EPI_SWIGLU, OUT_BF16)
 RGO_GEMM_EXTERN(false, EPI_GELU, OUT_BF16)
@@ -90,6 +91,7 @@ cudaError_t launch_gemm(const GemmJob& j, cudaStream_t s) {
     RGO_G(true, EPI_SWIGLU, OUT_E4M3)
     RGO_G(true, EPI_SWIGLU, OUT_BF16)
     RGO_G(true, EPI_GELU, OUT_E4M3)
+    RGO_G(true, EPI_GELU, OUT_BF16)
     RGO_G(false, EPI_NONE, OUT_BF16)
     RGO_G(false, EPI_SWIGLU, OUT_BF16)
     RGO_G(false, EPI_GELU, OUT_BF16)

@@ -234,4 +234,12 @@ int rgo_mask_load(const char* path, rgo_mask_desc* d, float* keep_prob, uint8_t*
     return RGO_OK;
 }
 
+uint64_t rgo_fnv1a64(const uint8_t* h_data, uint64_t n) {
+    // FNV-1a-64 (offset 0xcbf29ce484222325, prime 0x100000001b3): the checksum the
+    // golden mask fixtures carry (tests/golden/golden.json).
+    uint64_t h = 0xcbf29ce484222325ull;
+    for (uint64_t i = 0; i < n; ++i) h = (h ^ h_data[i]) * 0x100000001b3ull;
+    return h;
+}
+
 }  // extern "C"

@@ -81,6 +81,22 @@ __device__ __forceinline__ uint32_t keep32(uint64_t ctr0, uint32_t k0, uint32_t 
     return acc;
 }
 
+// keep32 with runtime rounds (any R in [1,16]): the in-GEMM queue's drain for
+// round counts without a compiled specialisation.
+__device__ __forceinline__ uint32_t keep32_rt(uint64_t ctr0, uint32_t k0, uint32_t k1, uint32_t thr,
+                                              int rounds) {
+    uint32_t acc = 0;
+#pragma unroll 1
+    for (int b = 0; b < 8; ++b) {
+        const uint64_t c = ctr0 + b;
+        const uint4 w = philox_rt(static_cast<uint32_t>(c), static_cast<uint32_t>(c >> 32), 0u, 0u, k0, k1, rounds);
+        acc |= (static_cast<uint32_t>(w.x < thr) | (static_cast<uint32_t>(w.y < thr) << 1) |
+                (static_cast<uint32_t>(w.z < thr) << 2) | (static_cast<uint32_t>(w.w < thr) << 3))
+               << (4 * b);
+    }
+    return acc;
+}
+
 // acc = 2*acc + (w >= thr) in two ALU-pipe ops (IADD3 carry-out, IADD3.X):
 // w - thr borrows exactly when w < thr, i.e. the carry-out is the DROP bit.
 // `zero` is an opaque 0 (kernel parameter): the third addend keeps ptxas

@@ -87,6 +87,29 @@ __device__ __forceinline__ void rng_drain_r(const RngQueue& q, const volatile in
     }
 }
 
+// Any round count (runtime loop; slower than the specialisations, same bits).
+__device__ __forceinline__ void rng_drain_rt(const RngQueue& q, const volatile int* stop, int stop_at) {
+    const uint32_t lane = threadIdx.x & 31;
+    while (true) {
+        if (stop && *stop >= stop_at) break;
+        unsigned long long start = 0;
+        if (lane == 0) start = atomicAdd(q.counter, 32ull);
+        start = __shfl_sync(0xffffffffu, start, 0);
+        if (start >= q.n_vec) break;
+        const uint64_t v = start + lane;
+        if (v < q.n_vec) {
+            const uint64_t ctr = q.base_offset + v * 32;
+            uint32_t w[4];
+#pragma unroll 1
+            for (int t = 0; t < 4; ++t) w[t] = rgo_dev::keep32_rt(ctr + 8 * t, q.k0, q.k1, q.thr, q.rounds);
+            uint8_t* p = q.out + v * 16;
+            asm volatile("st.global.cs.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(w[0]), "r"(w[1]), "r"(w[2]),
+                         "r"(w[3])
+                         : "memory");
+        }
+    }
+}
+
 __device__ __forceinline__ void rng_queue_drain(const RngQueue& q, const volatile int* stop, int stop_at = 4) {
     if (q.rounds == 10)
         rng_drain_r<10>(q, stop, stop_at);
@@ -96,7 +119,8 @@ __device__ __forceinline__ void rng_queue_drain(const RngQueue& q, const volatil
         rng_drain_r<5>(q, stop, stop_at);
     else if (q.rounds == 3)
         rng_drain_r<3>(q, stop, stop_at);
-    // other round counts are served by the tail kernel (rng_queue_kernel)
+    else
+        rng_drain_rt(q, stop, stop_at);
 }
 
 }  // namespace rgo

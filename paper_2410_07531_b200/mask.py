@@ -92,9 +92,13 @@ def desc(layout: MaskLayout, thr: KeepThreshold, rounds: int) -> _lib.mask_desc:
     )
 
 
-def generate_mask(layout: MaskLayout, thr: KeepThreshold, rounds: int, workers: int = 0) -> DropoutMask:
+def generate_mask(layout: MaskLayout, thr: KeepThreshold, rounds: int, workers: int = 0,
+                  shards: int = 0) -> DropoutMask:
     """generate_mask, mask.hpp:142-179, on the GPU.  `workers` maps to the
-    number of devices to shard over (0 = all); the bytes do not depend on it."""
+    number of devices to shard over (0 = all); `shards` (>= devices) splits
+    the mask into that many counter-offset shards, round-robin over the
+    devices starting at the current one.  The bytes depend on neither
+    (mask.hpp:139-141)."""
     layout.validate()
     if rounds < 1 or rounds > 16:
         raise ValueError("generate_mask: rounds must be in [1,16]")
@@ -104,8 +108,14 @@ def generate_mask(layout: MaskLayout, thr: KeepThreshold, rounds: int, workers: 
     if n > MAX_BITS:  # message produced by the C ABI (contains "bytes", "guard")
         _lib.check(_lib.lib().rgo_generate_mask_host(d, None, 0, 0))
     bits = np.empty(nbytes, dtype=np.uint8)
-    _lib.check(_lib.lib().rgo_generate_mask_host(d, bits.ctypes.data, nbytes, workers))
+    _lib.check(_lib.lib().rgo_generate_mask_host_ex(d, bits.ctypes.data, nbytes, workers, shards))
     return DropoutMask(dataclasses.replace(layout), thr.keep_prob, rounds, bits)
+
+
+def fnv1a64(data) -> int:
+    """FNV-1a-64 of a host byte buffer (numpy / CPU tensor) via the C ABI."""
+    arr = np.ascontiguousarray(data, dtype=np.uint8) if not hasattr(data, "numpy") else data.contiguous().numpy()
+    return int(_lib.lib().rgo_fnv1a64(arr.ctypes.data, arr.size))
 
 
 def generate_mask_device(layout: MaskLayout, thr: KeepThreshold, rounds: int, out=None,

@@ -246,10 +246,11 @@ def test_random_configs_modes_identical(rgo, cuda):
             assert torch.equal(outs[mode][1], want[: outs[mode][1].numel()]), (cfg, mode)
 
 
-@pytest.mark.parametrize("rounds", [5, 3])
+@pytest.mark.parametrize("rounds", [5, 3, 6, 12])
 def test_reduced_round_in_gemm_block(rgo, cuda, rounds):
-    """Philox-5/-3: the in-GEMM drains (and the matching inline-Philox baseline)
-    keep the modes bitwise equal and the mask equal to K1's."""
+    """Philox-5/-3 (compiled drains) and 6/12 (runtime-rounds drain): the
+    in-GEMM drains (and the matching inline-Philox baseline) keep the modes
+    bitwise equal and the mask equal to K1's."""
     import torch
     cfg = rgo.WorkloadConfig(batch=2, seq=512, heads=4, head_dim=128, ffn_dim=384, gated=True, keep_prob=0.9,
                              philox_rounds=rounds)
@@ -264,3 +265,21 @@ def test_reduced_round_in_gemm_block(rgo, cuda, rounds):
         assert torch.equal(v.view(torch.uint8), outs["serial_fused"][0][k].view(torch.uint8)), k
     want = rgo.generate_mask_device(rgo.MaskLayout(2, 4, 512, 9), rgo.KeepThreshold(0.9), rounds)
     assert torch.equal(outs["in_gemm"][1], want[: outs["in_gemm"][1].numel()])
+
+
+def test_block_rejects_threshold_edge_keep_prob(rgo, cuda):
+    """keep_prob 0.99999999 is < 1 as a double but 1.0f as the float the
+    reference stores (mask.hpp:59): threshold 2^32 cannot run through the
+    in-GEMM queue's 32-bit compare, so creation fails instead of the modes
+    silently disagreeing."""
+    cfg = small_cfg(rgo)
+    cfg.keep_prob = 0.99999999
+    for mode in ("serial_fused", "streams", "in_gemm"):
+        with pytest.raises(ValueError, match="threshold"):
+            rgo.Block(cfg, mode, seed=1)
+
+
+def test_block_rejects_bad_rng_warps(rgo, cuda):
+    cfg = small_cfg(rgo)
+    with pytest.raises(ValueError, match="RNG warps"):
+        rgo.Block(cfg, "in_gemm", seed=1, rng_launch=(0, 10, 0))

@@ -98,3 +98,37 @@ def test_element_source_carry(rgo):
     lay = rgo.MaskLayout(1, 4, 65536, 0, 0xFFFFFFFF)
     c, lane = rgo.element_source(lay, 1 << 33)
     assert lane == 0 and c.c1 == 1 and c.c0 == ((0xFFFFFFFF + (1 << 31)) & 0xFFFFFFFF)
+
+
+def _block_desc(rgo, keep_prob=0.9, rng_block=0):
+    d = rgo._lib.block_desc()
+    d.batch, d.seq, d.heads, d.head_dim, d.ffn, d.gated = 1, 256, 2, 128, 256, 1
+    d.keep_prob, d.rounds = keep_prob, 10
+    d.rng_launch = rgo._lib.launch(0, rng_block, 0, 0)
+    return d
+
+
+def test_block_create_validation(rgo):
+    """rgo_block_create rejects, before touching any buffer or device: a keep
+    probability whose float threshold is 2^32 or 0 (the in-GEMM queue's 32-bit
+    compare cannot express it), and an unsupported in-GEMM RNG-warp count."""
+    lib = rgo._lib.lib()
+    h = C.c_void_p()
+    bufs = rgo._lib.block_buffers()
+    for kp in (0.99999999, 1e-12):
+        assert lib.rgo_block_create(_block_desc(rgo, kp), bufs, 2, C.byref(h)) == rgo._lib.RGO_EINVAL
+        assert b"threshold" in lib.rgo_last_error()
+    for rw in (10, 256, 5):
+        assert lib.rgo_block_create(_block_desc(rgo, 0.9, rw), bufs, 2, C.byref(h)) == rgo._lib.RGO_EINVAL
+        assert b"RNG warps" in lib.rgo_last_error()
+    # the same launch shape is a mechanism-A (STREAMS) mask-kernel block size: not rejected there
+    assert lib.rgo_block_create(_block_desc(rgo, 0.9, 256), bufs, 1, C.byref(h)) == rgo._lib.RGO_EINVAL
+    assert b"missing buffer" in lib.rgo_last_error()
+
+
+def test_fnv1a64_via_capi(rgo, golden, mask_blobs):
+    """The C-ABI checksum equals the golden fixtures' FNV-1a-64."""
+    import numpy as np
+    for m in [x for x in golden["masks"] if x.get("blob")][:8]:
+        assert f"{rgo.mask.fnv1a64(mask_blobs[m['blob']]):016x}" == m["fnv"]
+    assert rgo.mask.fnv1a64(np.zeros(0, np.uint8)) == 0xcbf29ce484222325

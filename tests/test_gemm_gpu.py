@@ -66,6 +66,17 @@ def test_gelu_epilogue_fp8_out(rgo, cuda):
     assert rel(c.float(), ref.to(torch.float8_e4m3fn).float()) < 2e-2
 
 
+def test_gelu_epilogue_fp8_in_bf16_out(rgo, cuda):
+    """FP8 inputs + GELU + BF16 output (the GPT-3 block's ungated FFN1 with a bf16 result)."""
+    import torch
+    a = make((256, 512), torch.float32, 12, 2.0).to(torch.float8_e4m3fn)
+    b = make((512, 512), torch.float32, 13, 2.0).to(torch.float8_e4m3fn)
+    c = rgo.gemm(a, b, epilogue="gelu", alpha=1 / 32)
+    assert c.dtype == torch.bfloat16
+    ref = torch.nn.functional.gelu((a.float() @ b.float().T) / 32, approximate="tanh")
+    assert rel(c.float(), ref) < 5e-3
+
+
 @pytest.mark.parametrize("warps", [0, 4, 12, 16])
 def test_gemm_with_rng_mask_and_output(rgo, cuda, warps):
     """K4: co-resident RNG warps leave the GEMM result unchanged and, with the
@@ -88,7 +99,7 @@ def test_gemm_with_rng_mask_and_output(rgo, cuda, warps):
 
 def test_queue_drain_alone_matches_k1(rgo, cuda):
     import torch
-    for rounds in (7, 10, 5):
+    for rounds in (7, 10, 5, 1, 6, 16):
         lay = rgo.MaskLayout(2, 3, 512, 5, 0xFFFFFFFF - 300)
         thr = rgo.KeepThreshold(0.8)
         bits = torch.zeros(lay.elem_count() // 8, dtype=torch.uint8, device="cuda")
@@ -96,6 +107,25 @@ def test_queue_drain_alone_matches_k1(rgo, cuda):
         rgo.mask_queue_drain(rgo.mask.desc(lay, thr, rounds), bits, counter, grid=7)
         want = rgo.generate_mask_device(lay, thr, rounds)
         assert torch.equal(bits, want[: bits.numel()])
+
+
+@pytest.mark.parametrize("rounds", [6, 1, 16])
+def test_gemm_with_rng_runtime_rounds(rgo, cuda, rounds):
+    """Round counts without a compiled drain: the in-GEMM warps use the
+    runtime-rounds Philox and still produce K1's bits (no silent tail-only)."""
+    import torch
+    a, b = make((2048, 1024), torch.bfloat16, 14), make((1024, 1024), torch.bfloat16, 15)
+    lay = rgo.MaskLayout(1, 2, 512, 91, 77)
+    thr = rgo.KeepThreshold(0.85)
+    d = rgo.mask.desc(lay, thr, rounds)
+    bits = torch.zeros(lay.elem_count() // 8, dtype=torch.uint8, device="cuda")
+    counter = torch.zeros(1, dtype=torch.int64, device="cuda")
+    c = torch.empty(2048, 1024, dtype=torch.bfloat16, device="cuda")
+    rgo.gemm_with_rng(a, b, c, d, bits, counter, rng_warps=8)
+    torch.cuda.synchronize()
+    assert int(counter.item()) > 0  # the GEMM's RNG warps claimed work
+    rgo.mask_queue_drain(d, bits, counter)
+    assert torch.equal(bits, rgo.generate_mask_device(lay, thr, rounds)[: bits.numel()])
 
 
 def test_gemm_validation(rgo, cuda):

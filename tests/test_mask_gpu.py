@@ -116,3 +116,16 @@ def test_uniform_fill_matches_random_attention_input(rgo, cuda):
         want = oracle.uniform(42 ^ 0xA77E, stream, n)
         np.testing.assert_array_equal(f.cpu().numpy().view(np.uint32), want.view(np.uint32))
         np.testing.assert_array_equal(h.float().cpu().numpy(), torch.from_numpy(want).bfloat16().float().numpy())
+
+
+@pytest.mark.parametrize("shards", [2, 3, 7])
+def test_generate_mask_shards_one_device(rgo, cuda, shards):
+    """rgo_generate_mask_host's multi-shard slicing (per-shard counter offsets,
+    16-byte shard boundaries, ragged last shard) on one GPU: the bytes equal the
+    single-shard mask and the oracle's (mask.hpp:139-141 worker independence)."""
+    lay = rgo.MaskLayout(3, 5, 97, 11)
+    thr = rgo.KeepThreshold(0.75)
+    one = rgo.generate_mask(lay, thr, 7, workers=1).bits
+    many = rgo.generate_mask(lay, thr, 7, workers=1, shards=shards).bits
+    np.testing.assert_array_equal(many, one)
+    np.testing.assert_array_equal(one, oracle.generate_mask(3, 5, 97, 11, 0, 0.75, 7))
