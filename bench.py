@@ -105,9 +105,16 @@ def dist_setup():
         torch.cuda.set_device(dev)
         backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
         if backend == "nccl":
+            # communicator set-up visible in the log (ranks, NVLS/P2P transport); NCCL
+            # carries only the max-over-ranks timing scalars -- no data-path collective
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
         else:
             dist.init_process_group(backend)
+        t = torch.ones(1, device="cuda" if backend == "nccl" else "cpu")
+        dist.all_reduce(t)  # create the communicator now, outside any timed region
+        assert int(t.item()) == world
     else:
         torch.cuda.set_device(0)
     return rank, world, local
@@ -348,6 +355,87 @@ def run_block_modes(rgo, wl, rank, world, args, modes, chunks=1, passes=1):
     return blocks, res, samples, phases, launches
 
 
+class Energy:
+    """NVML total-energy counter (mJ) of the device this rank runs on."""
+
+    def __init__(self):
+        import torch
+        self.h = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            idx = torch.cuda.current_device()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            if vis:
+                idx = int(vis.split(",")[idx])
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.limit_w = pynvml.nvmlDeviceGetEnforcedPowerLimit(self.h) / 1e3
+            self.read()
+        except Exception:  # noqa: BLE001
+            self.h = None
+
+    def read(self):
+        return self.nv.nvmlDeviceGetTotalEnergyConsumption(self.h) / 1e3  # J
+
+    def sm_mhz(self):
+        return self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
+
+
+def bench_energy(blocks, modes, mask_fn, seconds=1.5):
+    """Energy per step of each mode (and of the stand-alone mask kernel), from
+    the NVML energy counter around ~`seconds` of back-to-back steps, with the
+    device time of the same run.  On a power-capped part time = energy / P, so
+    the RNG's exposed time should equal its extra energy over the cap:
+    (t_mode - t_no_rng) ~ (E_mode - E_no_rng) / P_cap."""
+    import torch
+    en = Energy()
+    if en.h is None:
+        return {"unavailable": "NVML energy counter not readable"}
+    out = {"power_limit_w": round(en.limit_w, 1)}
+    stream = torch.cuda.current_stream()
+
+    def run(fn, name):
+        for _ in range(5):
+            fn()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        n = max(20, int(seconds * 1e3 / e0.elapsed_time(e1)))
+        clocks = []
+        j0 = en.read()
+        e0.record(stream)
+        for i in range(n):
+            fn()
+            if i % max(1, n // 8) == 0:
+                clocks.append(en.sm_mhz())
+        e1.record(stream)
+        torch.cuda.synchronize()
+        j1 = en.read()
+        ms = e0.elapsed_time(e1) / n
+        joules = (j1 - j0) / n
+        out[name] = {"ms": round(ms, 4), "j_per_step": round(joules, 4), "avg_w": round(joules / ms * 1e3, 1),
+                     "sm_mhz_median": sorted(clocks)[len(clocks) // 2], "steps": n}
+
+    for m in modes:
+        run(blocks[m].step, m)
+    run(mask_fn, "mask_kernel")
+    if "no_rng" in out:
+        for m in modes:
+            if m == "no_rng":
+                continue
+            dt = out[m]["ms"] - out["no_rng"]["ms"]
+            de = out[m]["j_per_step"] - out["no_rng"]["j_per_step"]
+            out[m]["extra_ms_vs_no_rng"] = round(dt, 4)
+            out[m]["extra_j_vs_no_rng"] = round(de, 4)
+            out[m]["extra_j_over_cap_ms"] = round(de / en.limit_w * 1e3, 4)
+    return out
+
+
 def golden_mask_fnv(name, rounds):
     """The reference's FNV-1a-64 of the full mask (tests/golden/golden.json, recorded
     from the reference compiled in place, oracle/make_golden.py), or None."""
@@ -390,10 +478,47 @@ def block_parity(rgo, blocks, golden_name, rounds, rank):
     return out
 
 
+def measure_fp8_peak(seconds=4.0):
+    """Dense FP8 (e4m3 x e4m3 -> bf16) tensor peak of THIS GPU, measured like
+    MEASURED_PEAKS.json's bf16 figure: cuBLASLt through torch._scaled_mm at
+    8192^3 (2*N^3 flop), best of 10 (burst) and back to back for `seconds`
+    (sustained, i.e. at the power-capped clock a long step runs at)."""
+    import torch
+    N = 8192
+    a = torch.randn(N, N, device="cuda").to(torch.float8_e4m3fn)
+    b = torch.randn(N, N, device="cuda").to(torch.float8_e4m3fn).t()  # column-major operand
+    one = torch.ones((), device="cuda")
+
+    def mm():
+        return torch._scaled_mm(a, b, scale_a=one, scale_b=one, out_dtype=torch.bfloat16)
+    for _ in range(3):
+        mm()
+    best = float("inf")
+    for _ in range(10):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        mm()
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    iters = max(10, int(seconds * 1e3 / best))
+    e0.record()
+    for _ in range(iters):
+        mm()
+    e1.record()
+    torch.cuda.synchronize()
+    flop = 2.0 * N ** 3
+    del a, b
+    return {"fp8_tflops": round(flop / best / 1e9, 1),
+            "fp8_tflops_sustained": round(flop / (e0.elapsed_time(e1) / iters) / 1e9, 1),
+            "how": f"torch._scaled_mm e4m3 {N}^3 -> bf16: best of 10 (burst), {iters} back to back (sustained)"}
+
+
 def block_summary(rgo, wl, res, phases, mask_ms, peaks):
     gemm_flops = sum(g.flops() for g in rgo.gemm_shapes(wl))
     attn_flops = rgo.attention_work(wl)[0]
-    fp8_peak = 2 * peaks["bf16_tflops"]
+    fp8_peak = peaks["fp8_tflops"]
     roof_ms = gemm_flops / fp8_peak / 1e9 + attn_flops / peaks["bf16_tflops"] / 1e9
     best = min((m for m in ("streams", "in_gemm") if m in res), key=lambda m: res[m])
     value = res[best]
@@ -509,6 +634,31 @@ def bench_dropin_O(rgo, reps=20):
             "mask_fnv": f"{rgo.mask.fnv1a64(bits):016x}"}
 
 
+def bench_chunked(rgo, wl, rank, world, args, peaks, mask_ms_l):
+    import torch
+    out = {}
+    cmodes = ["serial_fused", "streams", "in_gemm", "no_rng"]
+    s32 = rgo.WorkloadConfig(batch=1, seq=32768, heads=32, head_dim=128, ffn_dim=11008, gated=True,
+                             keep_prob=0.9, philox_rounds=args.rounds)
+    for name, cfg, C in (("llama2_7b_C4", wl, 4), ("seq32k_C8", s32, 8)):
+        elems = cfg.batch * cfg.heads * cfg.seq ** 2
+        row = {"chunks": C, "full_mask_mib": elems // 8 // 2 ** 20, "live_mask_mib": 2 * elems // 8 // C // 2 ** 20,
+               "config": f"B{cfg.batch} nH{cfg.heads} SQ{cfg.seq} dH128 d4096 FFN11008 SwiGLU, keep 0.9, "
+                         f"Philox-{args.rounds}, {C} query-row windows"}
+        for label, chunks in (("chunked", C), ("unchunked", 1)):
+            blocks, res, _, ph, _ = run_block_modes(rgo, cfg, rank, world, args, cmodes, chunks=chunks)
+            for blk in blocks.values():
+                blk.close()
+            del blocks
+            torch.cuda.empty_cache()
+            row[f"{label}_modes_ms"] = {m: round(v, 4) for m, v in res.items()}
+            best = min(("streams", "in_gemm"), key=lambda m: res[m])
+            row[f"{label}_best"] = best
+            row[f"{label}_speedup_vs_fused"] = round(res["serial_fused"] / res[best], 4)
+        out[name] = row
+    return out
+
+
 def bench_gemms(rgo, wl, world, peaks):
     import torch
     f8 = torch.float8_e4m3fn
@@ -525,11 +675,11 @@ def bench_gemms(rgo, wl, world, peaks):
         tot_flop += sh.flops()
         tot_ms += ms
         del a, b, c
-    peak = 2 * peaks["bf16_tflops"]
+    peak = peaks["fp8_tflops"]
     ach = tot_flop / tot_ms / 1e9
     return {"bound": "tensor", "achieved": round(ach, 1), "peak": round(peak, 1), "unit": "TFLOP/s",
             "frac": round(ach / peak, 4), "per_gemm": out,
-            "note": "FP8 peak = 2 x measured bf16 (derived); stand-alone, not power-capped by the rest of the step"}
+            "note": "FP8 peak measured in this run (cuBLASLt e4m3 8192^3 burst, fp8_peak); stand-alone GEMMs"}
 
 
 def event_ms(fn, reps, world, warm=1):
@@ -647,6 +797,9 @@ def bench_block(args, rank, world):
     elems = cfg["batch"] * cfg["heads"] * cfg["seq"] ** 2
     modes = ["serial_fused", "streams", "in_gemm", "no_rng"]
     peaks, src = load_peaks()
+    log("FP8 peak (cuBLASLt e4m3 8192^3)")
+    fp8 = measure_fp8_peak()
+    peaks.update(fp8_tflops=fp8["fp8_tflops"], fp8_tflops_sustained=fp8["fp8_tflops_sustained"])
     log("Llama2-7B block modes")
     with ClockSampler(torch.cuda.current_device()) as clk:
         blocks, res, samples, phases, launches = run_block_modes(rgo, wl, rank, world, args, modes, passes=3)
@@ -657,6 +810,12 @@ def bench_block(args, rank, world):
     mask_ms = max_over_ranks(mask_ms, world)
     best, value, summ = block_summary(rgo, wl, res, phases, mask_ms, peaks)
     parity = block_parity(rgo, blocks, "L", cfg["rounds"], rank)
+    log("energy per mode (NVML)")
+    lay_l = rgo.MaskLayout(cfg["batch"], cfg["heads"], cfg["seq"], 42, blocks["in_gemm"].desc.base_offset)
+    mask_buf = torch.empty(elems // 8, dtype=torch.uint8, device="cuda")
+    energy = bench_energy(blocks, modes, lambda: rgo.generate_mask_device(lay_l, rgo.KeepThreshold(cfg["keep_prob"]),
+                                                                          cfg["rounds"], out=mask_buf))
+    del mask_buf
     # ----- e2e through the public API with host buffers.  A step's input is the
     # previous block's attention output (`attn_in`, bf16 [M, d], 128 MiB, read by the
     # step's first kernel) and its result is this block's attention output (`attn_o`,
@@ -706,8 +865,10 @@ def bench_block(args, rank, world):
                          "hbm_write_gbs": round(elems / 8 / (mask_ms * 1e-3) / 1e9, 1)},
         "blocks_per_s": round(world * 1e3 / value, 3),
         "block_roofline": dict(summ["block_roofline"],
-                               **{"def": f"sum(GEMM flop)/FP8 peak + attention flop/BF16 peak; FP8 peak = 2 x "
-                                         f"measured bf16 {bf16_peak} TF/s ({src})"}),
+                               **{"def": f"sum(GEMM flop)/FP8 peak + attention flop/BF16 peak; FP8 peak "
+                                         f"{peaks['fp8_tflops']} TF/s measured in this run (fp8_peak), bf16 "
+                                         f"{bf16_peak} TF/s ({src})"}),
+        "fp8_peak": fp8,
         "roofline": {"bound": "tensor", "kernel": "attention fwd (mask bits), in situ (no-RNG step phase)",
                      "achieved": round(attn_flops / (att_ms * 1e-3) / 1e12, 2), "peak": bf16_peak,
                      "unit": "TFLOP/s", "frac": round(attn_flops / (att_ms * 1e-3) / 1e12 / bf16_peak, 4),
@@ -721,6 +882,7 @@ def bench_block(args, rank, world):
                        "D2H stream; two replicas alternate so copies overlap neighbouring steps; the timed "
                        "region ends when the last result is in host memory"},
         "parity": parity,
+        "energy": energy,
         "clocks": clocks, "gpu_launches": launches[best],
     }
     if not args.no_extras:
@@ -761,18 +923,12 @@ def bench_block(args, rank, world):
                                             "Philox-10; RNG hidden under 2 + 16 expert GEMMs"}, **msum)
         # batch-chunk pipelining of RNG -> GEMMs -> attention (schedule.hpp:206-239):
         # 4 chunks of one batch item each, live mask = 2 x 64 MiB instead of 256 MiB
-        log("chunked pipeline")
-        cmodes = ["serial_fused", "streams", "no_rng"]
-        cblocks, cres, _, cph, _ = run_block_modes(rgo, wl, rank, world, args, cmodes, chunks=4)
-        for blk in cblocks.values():
-            blk.close()
-        del cblocks
-        torch.cuda.empty_cache()
-        _, cval, csum = block_summary(rgo, wl, cres, cph, mask_ms, peaks)
-        line["chunked_pipeline"] = dict({"value_ms": round(cval, 4), "chunks": 4,
-                                         "live_mask_mib": 2 * elems // 8 // 4 // 2 ** 20,
-                                         "config": "Llama2-7B block, batch split into 4 pipeline stages (mechanism A "
-                                                   "per stage, 2-slot mask ring)"}, **csum)
+        # SQ-chunk pipelining (pipeline_schedule, schedule.hpp:205-239): query-row
+        # windows, stage c = attention(c) -> GEMMs of window c with window c+1's RNG hidden under
+        # them; live mask = 2 windows.  Llama2-7B (C = 4) and the long-context config S
+        # (B1 nH32 SQ32K, C = 8: 1 GiB live instead of 4 GiB), against the unchunked step.
+        log("SQ-chunk pipeline")
+        line["chunked_pipeline"] = bench_chunked(rgo, wl, rank, world, args, peaks, mask_ms)
         log("attention fwd+bwd")
         line["attention_fwd_bwd"] = bench_attention_bwd(rgo, rank, world, peaks)
         log("flash-attn library baseline")
@@ -876,13 +1032,14 @@ def main():
         vals = [cpu_reference_block(cfg) for _ in range(steps)]
         v = sum(x["value"] for x in vals) / len(vals)
         b = vals[-1]
+        suite = cpu_baseline_suite(args.rounds)
         print(json.dumps({
             "metric": "llama2_block_ms", "value": round(v, 1), "unit": "ms", "n_gpus": 0, "impl": "reference",
             "steps": steps, "warmup": 0, "higher_is_better": False, "scaling": "weak",
             "config": {"workload": "Llama2-7B block (reference CPU path: generate_mask + attention_dropout_fused; "
                                    "no GEMMs in the reference)", "global_batch": cfg["batch"], "seq_len": cfg["seq"]},
             "cpu_baseline": {"value": round(v, 1), "unit": "ms", "cores": b["cores"], "kind": b["kind"],
-                             "sample": b["sample"]},
+                             "sample": b["sample"], "host": suite["host"], "suite": suite},
             "e2e": {"value": round(v, 1), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
         return
 
@@ -902,6 +1059,10 @@ def main():
     if args.watchdog_s > 0:
         wd.start()
     line = bench_block(args, rank, world) if args.workload == "block" else bench_mask_only(args, rank, world)
+    if rank == 0 and args.workload == "block":
+        import paper_2410_07531_b200 as rgo
+        log("drop-in e2e at config O (host arrays through the C ABI)")
+        line["e2e_dropin_O"] = bench_dropin_O(rgo)
     wd.cancel()
     if rank == 0:
         if not args.no_cpu_baseline and world == 1:  # the CPU baseline is an N=1 measurement
@@ -909,6 +1070,17 @@ def main():
             cb = cpu_reference_block(dict(L, rounds=args.rounds))
             line["cpu_baseline"] = {k: (round(cb[k], 1) if k == "value" else cb[k])
                                     for k in ("value", "unit", "cores", "kind", "sample")}
+            log("CPU baseline suite (BASELINE.md section 4)")
+            suite = cpu_baseline_suite(args.rounds)
+            line["cpu_baseline"]["host"] = suite["host"]
+            line["cpu_baseline"]["suite"] = suite
+            if "e2e_dropin_O" in line:
+                ref_ms = (suite["masks"]["O"]["s"] + suite["attention_O"]["decoupled_s_1thread"]) * 1e3
+                line["e2e_dropin_O"]["reference_cpu_ms"] = round(ref_ms, 3)
+                line["e2e_dropin_O"]["reference_cpu_how"] = (
+                    "the reference's generate_mask (all threads) + attention_dropout_decoupled (single thread, as "
+                    "the reference runs it) at config O, same host")
+                line["e2e_dropin_O"]["speedup_vs_reference_cpu"] = round(ref_ms / line["e2e_dropin_O"]["value_ms"], 2)
         print(json.dumps(line))
         if "parity" in line and not line["parity"]["ok"]:
             log(f"PARITY FAILURE: {line['parity']}")

@@ -289,9 +289,14 @@ typedef struct rgo_block_desc {
                                RNG warps per GEMM CTA (4/6/8/12/16, 0 = chosen per workload) */
     uint32_t experts;       /* 0: dense FFN; > 0: MoE with `experts` expert FFNs of width ffn */
     uint32_t top_k;         /* MoE: experts per token (balanced synthetic routing) */
-    uint32_t chunks;        /* > 1: pipeline the step over `chunks` batch groups (dense FFN, modes
-                               SERIAL_FUSED / STREAMS / NO_RNG); the mask buffer is then a 2-slot
-                               ring of chunk masks (schedule.hpp:206-239, capacity.hpp:51-59) */
+    uint32_t chunks;        /* > 1: SQ-chunk pipeline (schedule.hpp:205-239, capacity.hpp:51-59):
+                               the query rows of every sequence split into `chunks` windows
+                               (seq/chunks % 128 == 0, dense FFN, every mode); a step is the
+                               rotation [attention(c) -> Proj/FFN1/FFN2/QKV of window c] for
+                               c = 0..chunks-1, reading qkv and writing qkv_out, with window c+1's
+                               mask hidden under stage c's GEMMs.  The mask buffer is a 2-slot
+                               ring of window masks [slice][seq/chunks][seq] (2/chunks of the full
+                               mask); counter needs `chunks` entries (IN_GEMM) */
     uint32_t reserved2;
 } rgo_block_desc;
 
@@ -313,6 +318,7 @@ typedef struct rgo_block_buffers {
     void* xd;       /* MoE: e4m3 [M*top_k, d] dispatched expert inputs (NULL when dense) */
     void* ye;       /* MoE: bf16 [M*top_k, d] expert outputs (NULL when dense) */
     const void* attn_in; /* bf16 [M, d] step input; NULL = attn_o (steps chained through it) */
+    void* qkv_out;  /* chunked step: bf16 [M, 3d] the step's QKV output (NULL when unchunked) */
 } rgo_block_buffers;
 
 typedef struct rgo_block rgo_block;

@@ -94,7 +94,7 @@ class block_buffers(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in ("x", "wqkv", "wo", "w1", "w2", "qkv", "attn_o", "attn_o8", "y1", "h",
                                           "mask")] + [("mask_bytes", C.c_uint64), ("counter", C.c_void_p),
                                                       ("lse", C.c_void_p), ("xd", C.c_void_p), ("ye", C.c_void_p),
-                                                      ("attn_in", C.c_void_p)]
+                                                      ("attn_in", C.c_void_p), ("qkv_out", C.c_void_p)]
 
 
 # name -> (restype, argtypes).  Every symbol include/rgo/capi.h declares.

@@ -32,8 +32,12 @@ class Block:
     def __init__(self, cfg: WorkloadConfig, mode: str = "streams", seed: int = 42, base_offset: int = 0,
                  rng_launch=(0, 0, 0), use_graph: bool = True, device="cuda", weights=None, chunks: int = 1,
                  chained: bool = False):
-        """chunks > 1: pipeline the step over `chunks` batch groups (schedule.hpp:206-239);
-        the mask buffer is then a 2-slot ring of chunk masks.  chained=False (default):
+        """chunks > 1: SQ-chunk pipeline (pipeline_schedule, schedule.hpp:205-239): the
+        query rows of every sequence split into `chunks` windows; a step is the rotation
+        [attention(c) -> Proj/FFN1/FFN2/QKV of window c] over c, reading `qkv` (the
+        previous step's QKV output) and writing `qkv_out`, with window c+1's mask hidden
+        under stage c's GEMMs; the mask buffer is a 2-slot ring of window masks
+        [slice][seq/chunks][seq] (2/chunks of the full mask).  chained=False (default):
         every step reads the same stationary input `attn_in` (unit-variance synthetic
         data); chained=True: each step consumes the previous step's attention output,
         which -- without the LayerNorm/residuals the reference also omits -- drifts to
@@ -65,18 +69,21 @@ class Block:
         self.chunks = max(1, chunks)
         live = elems if self.chunks == 1 else 2 * (elems // self.chunks)
         self.mask = torch.zeros(live // 8, dtype=torch.uint8, device=dev)
-        if mode == "no_rng":
+        self.qkv_out = torch.empty(M, 3 * d, dtype=bf, device=dev) if self.chunks > 1 else None
+        if self.chunks > 1:
+            # the chunked step's input QKV: a deterministic synthetic stand-in for the
+            # previous step's output (unit-variance Q/K/V), overwritten by callers at will
+            self.qkv.copy_(_uniform(M * 3 * d, 10, seed, dev).view(M, 3 * d).mul_(math.sqrt(3.0)).to(bf))
+        if mode == "no_rng" and self.chunks == 1:
             # NO_RNG never writes the mask; give its attention the real keep pattern
             # (an all-zero mask would feed the tensor cores zeros -- less power, higher
-            # clock -- and make this measurement floor optimistic)
+            # clock -- and make this measurement floor optimistic).  Chunked: the
+            # runtime primes both ring slots with windows 0 and 1 on the first step.
             from .mask import MaskLayout, generate_mask_device
-            n_slices = B * H if self.chunks == 1 else (B // self.chunks) * H
-            lay = MaskLayout(1, n_slices, S, seed, base_offset)
-            for c in range(1 if self.chunks == 1 else 2):
-                part = self.mask[c * (live // 8 // (1 if self.chunks == 1 else 2)):]
-                generate_mask_device(lay, KeepThreshold(cfg.keep_prob), cfg.philox_rounds, out=part[: lay.elem_count() // 8])
+            lay = MaskLayout(B, H, S, seed, base_offset)
+            generate_mask_device(lay, KeepThreshold(cfg.keep_prob), cfg.philox_rounds, out=self.mask)
             torch.cuda.synchronize()
-        self.counter = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.counter = torch.zeros(max(1, self.chunks), dtype=torch.int64, device=dev)
         self.lse = None
         # weights U(-1,1) (variance 1/3): alpha = sqrt(3/K) keeps activations at unit
         # variance; a chained step's input is an attention output (~0.1-0.3): s_attn 8
@@ -100,7 +107,8 @@ class Block:
                                   self.attn_o8.data_ptr(), self.y1.data_ptr(), self.h.data_ptr(),
                                   self.mask.data_ptr(), self.mask.numel(), self.counter.data_ptr(), None,
                                   self.xd.data_ptr() if E else None, self.ye.data_ptr() if E else None,
-                                  None if chained else self.attn_in.data_ptr())
+                                  None if chained else self.attn_in.data_ptr(),
+                                  self.qkv_out.data_ptr() if self.qkv_out is not None else None)
         self._bufs = bufs
         handle = C.c_void_p()
         torch.cuda.synchronize()

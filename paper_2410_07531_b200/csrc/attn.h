@@ -8,8 +8,11 @@ namespace rgo_attn {
 enum { MASK_NONE = 0, MASK_BITS = 1, MASK_PHILOX = 2 };
 
 struct AttnParams {
-    int B, H, S;
-    int n_pairs;             // ceil(S / 256): CTAs per (b, h)
+    int B, H, S;             // S = keys per slice (the layout's SQ)
+    int Sq;                  // query rows of this launch per slice (S, or a pipeline chunk's rows)
+    int q_row0;              // global row of query 0 (mask counters, LSE): 0, or the chunk's first row
+    int bits_rows;           // MASK_BITS: rows per slice in `bits` (S: full layout; Sq: a chunk's mask)
+    int n_pairs;             // ceil(Sq / 256): CTAs per (b, h)
     float scale_log2;        // log2(e) / sqrt(head_dim)
     float keep_prob;         // float keep probability (1 for no dropout)
     const uint8_t* bits;     // MASK_BITS: packed mask, reference layout
@@ -42,6 +45,13 @@ struct AttnOut {
 
 struct AttnJob {
     int B, H, S, HD;         // HD in {64, 128}
+    // Query-row window (SQ-chunk pipelining, schedule.hpp:205-239): rows
+    // [q_row0, q_row0 + Sq) of every slice attend over all S keys; q and o
+    // point at row q_row0.  Sq = 0 means the whole sequence.  bits_rows: rows
+    // per slice held in `bits` (0 = S: the full layout, read at row q_row0;
+    // Sq: a compact chunk mask [slice][Sq][S]).  Keep bits / Philox counters
+    // are the full layout's: element (s*S + q_row0 + i)*S + j.
+    int Sq, q_row0, bits_rows;
     float scale;             // 1/sqrt(true head_dim)
     AttnTensor q, k, v;
     AttnOut o;

@@ -326,12 +326,17 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(const __grid_const
         const uint32_t q = warp & 3;
         const int row = q * 32 + lane;
         const int i = q0 + w * BQ + row;  // query index within the slice
-        const bool row_valid = i < p.S;
+        const bool row_valid = i < p.Sq;
         const uint32_t lane_base = (q * 32) << 16;
         const uint32_t tS = tmem + lane_base + w * 128;
         const uint32_t tO = tmem + lane_base + 256 + w * 128;
         const uint64_t slice = static_cast<uint64_t>(bb) * p.H + hh;
-        const uint64_t row_base = (slice * p.S + static_cast<uint64_t>(row_valid ? i : 0)) * p.S;
+        // bits index (MASK_BITS: the buffer's own row layout) and global element
+        // index (MASK_PHILOX: the full layout's counters) of key 0 of this row
+        const uint64_t ri = static_cast<uint64_t>(row_valid ? i : 0);
+        const uint64_t row_base = MODE == MASK_BITS
+                                      ? (slice * p.bits_rows + ri + (p.bits_rows == p.S ? p.q_row0 : 0)) * p.S
+                                      : (slice * p.S + p.q_row0 + ri) * p.S;
         float m = -INFINITY, l = 0.0f;
         // MASK_BITS: the 16 bytes of tile j+1 are loaded while tile j is processed
         uint32_t kw_next[4] = {0u, 0u, 0u, 0u};
@@ -464,7 +469,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(const __grid_const
                     dst[v] = make_uint4(packed[4 * v], packed[4 * v + 1], packed[4 * v + 2], packed[4 * v + 3]);
             }
         }
-        if (p.lse && row_valid) p.lse[slice * p.S + i] = (m + __log2f(l)) * 0.6931471805599453f;
+        if (p.lse && row_valid) p.lse[slice * p.S + p.q_row0 + i] = (m + __log2f(l)) * 0.6931471805599453f;
     }
     __syncthreads();
     if (warp == 1) tmem_dealloc<TMEM_COLS>(tmem);
@@ -506,12 +511,18 @@ static bool tmap_qkv(CUtensorMap* m, const AttnTensor& t, int B, int H, int S, i
 cudaError_t launch_attn_fwd(const AttnJob& j, cudaStream_t s) {
     using namespace rgo_attn;
     CUtensorMap tq, tk, tv;
-    if (!tmap_qkv(&tq, j.q, j.B, j.H, j.S, j.HD) || !tmap_qkv(&tk, j.k, j.B, j.H, j.S, j.HD) ||
+    const int Sq = j.Sq > 0 ? j.Sq : j.S;
+    if (j.q_row0 < 0 || j.q_row0 + Sq > j.S) return cudaErrorInvalidValue;
+    if (!tmap_qkv(&tq, j.q, j.B, j.H, Sq, j.HD) || !tmap_qkv(&tk, j.k, j.B, j.H, j.S, j.HD) ||
         !tmap_qkv(&tv, j.v, j.B, j.H, j.S, j.HD))
         return cudaErrorInvalidValue;
     AttnParams p{};
     p.B = j.B; p.H = j.H; p.S = j.S;
-    p.n_pairs = (j.S + 2 * BQ - 1) / (2 * BQ);
+    p.Sq = Sq;
+    p.q_row0 = j.q_row0;
+    p.bits_rows = j.bits_rows > 0 ? j.bits_rows : j.S;
+    if (p.bits_rows != j.S && p.bits_rows != Sq) return cudaErrorInvalidValue;
+    p.n_pairs = (Sq + 2 * BQ - 1) / (2 * BQ);
     p.scale_log2 = j.scale * 1.4426950408889634f;
     p.keep_prob = j.mode == MASK_NONE ? 1.0f : j.keep_prob;
     p.bits = j.bits;

@@ -62,6 +62,34 @@ __global__ void quant_e4m3_kernel(const __nv_bfloat16* __restrict__ in, uint8_t*
     }
 }
 
+// Row-mapped variant for the SQ-chunk pipeline: row r of the window lives at
+// (r / rb) * rstride + roff + r % rb of both in and out (d % 16 == 0).
+__global__ void quant_e4m3_rows_kernel(const __nv_bfloat16* __restrict__ in, uint8_t* __restrict__ out, int rows,
+                                       int d, int rb, int rstride, int roff, float scale) {
+    const int vec = d / 16;
+    const uint64_t n = static_cast<uint64_t>(rows) * vec;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const int r = static_cast<int>(i / vec), c = static_cast<int>(i % vec);
+        const uint64_t off = static_cast<uint64_t>((r / rb) * rstride + roff + r % rb) * d + 16 * c;
+        const uint4 a = *reinterpret_cast<const uint4*>(in + off);
+        const uint4 b = *reinterpret_cast<const uint4*>(in + off + 8);
+        const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+        uint32_t o[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const float2 f0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[2 * k]));
+            const float2 f1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[2 * k + 1]));
+            const __nv_fp8x2_storage_t lo = __nv_cvt_float2_to_fp8x2(make_float2(f0.x * scale, f0.y * scale),
+                                                                     __NV_SATFINITE, __NV_E4M3);
+            const __nv_fp8x2_storage_t hi = __nv_cvt_float2_to_fp8x2(make_float2(f1.x * scale, f1.y * scale),
+                                                                     __NV_SATFINITE, __NV_E4M3);
+            o[k] = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
+        }
+        *reinterpret_cast<uint4*>(out + off) = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+}
+
 // MoE dispatch: row y1[t] -> xd[slot(t, j)] for every token-expert pair
 // p = t*k + j (expert p % E, row p / E of its slice).  16 bytes per thread.
 __global__ void moe_dispatch_kernel(const uint8_t* __restrict__ y1, uint8_t* __restrict__ xd, int M, int d, int k,
@@ -133,6 +161,15 @@ cudaError_t launch_quant_e4m3(const void* in, void* out, uint64_t n, float scale
     return cudaGetLastError();
 }
 
+cudaError_t launch_quant_e4m3_rows(const void* in, void* out, int rows, int d, int rb, int rstride, int roff,
+                                   float scale, cudaStream_t s) {
+    if (d % 16 || rb <= 0) return cudaErrorInvalidValue;
+    const uint64_t items = static_cast<uint64_t>(rows) * (d / 16);
+    rgo_dev::quant_e4m3_rows_kernel<<<stream_grid(items), 256, 0, s>>>(
+        static_cast<const __nv_bfloat16*>(in), static_cast<uint8_t*>(out), rows, d, rb, rstride, roff, scale);
+    return cudaGetLastError();
+}
+
 struct Block {
     BlockConfig cfg;
     BlockBuffers buf;
@@ -149,6 +186,7 @@ struct Block {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     int launches_per_step = 0;
+    bool primed = false;  // chunked: window 0's mask (and window 1's for NO_RNG) generated
 };
 
 static bool block_pdl() {  // RGO_BLOCK_PDL=0 turns programmatic dependent launch off (A/B)
@@ -157,6 +195,16 @@ static bool block_pdl() {  // RGO_BLOCK_PDL=0 turns programmatic dependent launc
         return !(e && e[0] == '0');
     }();
     return on;
+}
+
+// Programmatic dependent launch inside the chunked pipeline's stages
+// (RGO_CHUNK_PDL=1; default off until stress-tested).
+static bool chunk_pdl() {
+    static const bool on = [] {
+        const char* e = getenv("RGO_CHUNK_PDL");
+        return e && e[0] == '1';
+    }();
+    return on && block_pdl();
 }
 
 static GemmJob gemm(const BlockConfig& c, int M, int N, int K, const void* A, const void* B, void* C, int epi,
@@ -339,108 +387,155 @@ static cudaError_t enqueue_step(Block& b, int* launches) {
     return cudaSuccess;
 }
 
-// Chunked step (chunks > 1): the batch is split into `chunks` groups of Bc
-// items.  Stage c = quant + Proj/FFN1/FFN2/QKV on the group's M/chunks rows
-// and the attention of the group; in STREAMS mode the group's mask (the
-// contiguous slices [c*Bc*H, (c+1)*Bc*H) of the full layout, counter base
-// base_offset + c*Bc*H*S^2/4) is generated on the low-priority stream into
-// ring slot c % 2 while the group's GEMMs run, so at most two chunk masks are
-// live (one being read by attention(c-1)'s tail, one being written).
-// Results are bitwise those of the unchunked step (row-tiled GEMMs and
-// per-slice attention do not depend on the grouping).
+// SQ-chunk pipelined step (chunks = C > 1; pipeline_schedule, schedule.hpp:205-239;
+// PAPER.md:254-261): the query rows of every sequence are split into C windows
+// of Sc = SQ/C rows.  One step is the C-stage rotation
+//     for c: attention(c)  ->  quant + Proj + FFN1 + FFN2 + QKV on window c's rows
+// Attention(c) reads the step's input QKV (qkv: Q rows of window c, all keys)
+// and the window's compact mask [slice][Sc][SQ] from ring slot c % 2; stage c's
+// GEMMs (M = B*Sc rows, row blocks of Sc every SQ rows) write window c of qkv_out.
+// The mask of window c+1 (window 0 of the next step after the last stage) is
+// generated while stage c's GEMMs run -- by K1 on the low-priority stream
+// (STREAMS, after attention(c) has released the slot) or by the GEMMs'
+// co-resident RNG warps + tail (IN_GEMM) -- so at most two window masks are live
+// (2/C of the full mask; capacity.hpp:51-59).  Every keep bit and Philox counter is
+// the full layout's, so attention(c) equals rows [c*Sc, (c+1)*Sc) of the
+// unchunked attention bitwise, and the row-tiled GEMMs equal the unchunked
+// GEMMs' rows bitwise.
 static cudaError_t enqueue_step_chunked(Block& b, int* launches) {
     const BlockConfig& c = b.cfg;
     const BlockBuffers& x = b.buf;
-    const int C = c.chunks, Bc = c.batch / C;
-    const int M = c.batch * c.seq, Mc = Bc * c.seq, d = c.heads * c.head_dim, F = c.ffn;
+    const int C = c.chunks, S = c.seq, Sc = S / C;
+    const int M = c.batch * S, Mc = c.batch * Sc, d = c.heads * c.head_dim, F = c.ffn;
     const int n1 = c.gated ? 2 * F : F;
-    const uint64_t chunk_elems = static_cast<uint64_t>(Bc) * c.heads * c.seq * static_cast<uint64_t>(c.seq);
-    const uint64_t chunk_bytes = chunk_elems / 8;
+    const uint64_t win_elems = static_cast<uint64_t>(c.batch) * c.heads * Sc * static_cast<uint64_t>(S);
+    const uint64_t win_bytes = win_elems / 8;
     cudaStream_t s = b.s_main;
     int n = 0;
     cudaError_t e;
-    (void)M;
     if ((e = record_timing(b, 0, s)) != cudaSuccess) return e;
-    if (b.mode == BLOCK_STREAMS) {
-        if ((e = cudaEventRecord(b.ev_fork, s)) != cudaSuccess) return e;
-        if ((e = cudaStreamWaitEvent(b.s_rng, b.ev_fork, 0)) != cudaSuccess) return e;
-    }
-    auto rows8 = [&](const void* base, int row, int ld) {
-        return static_cast<const uint8_t*>(base) + static_cast<uint64_t>(row) * ld;
+    if (b.mode == BLOCK_IN_GEMM &&
+        (e = cudaMemsetAsync(x.counter, 0, sizeof(unsigned long long) * C, s)) != cudaSuccess)
+        return e;
+    auto queue_for = [&](int w) {  // work queue of window w's mask into slot w % 2
+        RngQueue q{};
+        q.out = x.mask + (w & 1) * win_bytes;
+        q.n_vec = win_elems / 128;
+        q.base_offset = c.base_offset;
+        q.k0 = static_cast<uint32_t>(c.seed);
+        q.k1 = static_cast<uint32_t>(c.seed >> 32);
+        q.thr = static_cast<uint32_t>(c.threshold);
+        q.rounds = c.rounds;
+        q.counter = x.counter + w;
+        q.win = make_window(static_cast<uint32_t>(Sc), static_cast<uint32_t>(w * Sc), static_cast<uint32_t>(S));
+        return q;
     };
+    const int rw = c.rng_block ? static_cast<int>(c.rng_block) : auto_rng_warps(c);
+    const long long ld = 3LL * d;
     for (int ch = 0; ch < C; ++ch) {
-        const int slot = ch & 1;
-        uint8_t* bits = x.mask + slot * chunk_bytes;
-        const uint64_t base = c.base_offset + static_cast<uint64_t>(ch) * (chunk_elems / 4);
-        if (b.mode == BLOCK_STREAMS) {
-            // mask of chunk ch starts when attention(ch-1) ends: it overlaps the
-            // chunk's GEMMs only (sharing SMs with the MUFU-bound attention
-            // slows both), and slot ch % 2 (last read by attention(ch-2)) is free
-            if (ch >= 1 && (e = cudaStreamWaitEvent(b.s_rng, b.ev_slot[ch - 1], 0)) != cudaSuccess) return e;
-            MaskJob mj{bits, chunk_elems, c.seed, base, c.threshold, c.rounds};
+        const int nxt = (ch + 1) % C;  // window whose mask this stage's GEMMs hide
+        const int r0 = ch * Sc;
+        if (b.mode == BLOCK_STREAMS && ch > 0 && (e = cudaStreamWaitEvent(s, b.ev_chunk[ch], 0)) != cudaSuccess)
+            return e;
+        AttnJob a{};
+        a.B = c.batch; a.H = c.heads; a.S = S; a.HD = c.head_dim;
+        a.Sq = Sc;
+        a.q_row0 = r0;
+        a.bits_rows = Sc;
+        a.scale = 1.0f / sqrtf(static_cast<float>(c.head_dim));
+        const __nv_bfloat16* qkv = static_cast<const __nv_bfloat16*>(x.qkv);
+        a.q = {qkv + static_cast<long long>(r0) * ld, static_cast<long long>(S) * ld, c.head_dim, ld};
+        a.k = {qkv + d, static_cast<long long>(S) * ld, c.head_dim, ld};
+        a.v = {qkv + 2 * d, static_cast<long long>(S) * ld, c.head_dim, ld};
+        a.o = {static_cast<__nv_bfloat16*>(x.attn_o) + static_cast<long long>(r0) * d, static_cast<long long>(S) * d,
+               c.head_dim, d};
+        a.lse = x.lse;
+        a.mode = b.mode == BLOCK_SERIAL_FUSED ? rgo_attn::MASK_PHILOX : rgo_attn::MASK_BITS;
+        a.keep_prob = c.keep_prob;
+        a.bits = x.mask + (ch & 1) * win_bytes;
+        a.bits_bytes = win_bytes;
+        a.seed = c.seed;
+        a.base_offset = c.base_offset;
+        a.threshold = c.threshold;
+        a.rounds = c.rounds;
+        // programmatic dependent of the previous stage's tail drain / QKV GEMM (not across
+        // the STREAMS event join, and not for the step's first kernel)
+        a.pdl = chunk_pdl() && ch > 0 && b.mode != BLOCK_STREAMS;
+        if ((e = launch_attn_fwd(a, s)) != cudaSuccess) return e;
+        ++n;
+        if (b.mode == BLOCK_STREAMS) {  // window nxt's mask: after attention(ch) released slot nxt % 2
+            if ((e = cudaEventRecord(b.ev_slot[ch], s)) != cudaSuccess) return e;
+            if ((e = cudaStreamWaitEvent(b.s_rng, b.ev_slot[ch], 0)) != cudaSuccess) return e;
+            MaskJob mj{x.mask + (nxt & 1) * win_bytes, win_elems, c.seed, c.base_offset, c.threshold, c.rounds};
+            mj.win_rows = static_cast<uint32_t>(Sc);
+            mj.row0 = static_cast<uint32_t>(nxt * Sc);
+            mj.seq = static_cast<uint32_t>(S);
             LaunchShape ls;
             ls.grid = c.rng_grid ? c.rng_grid : static_cast<unsigned>(num_sms());
             ls.block = c.rng_block ? c.rng_block : 256;
             ls.dyn_smem = c.rng_smem;
             if ((e = launch_mask(mj, ls, b.s_rng)) != cudaSuccess) return e;
             ++n;
-            if ((e = cudaEventRecord(b.ev_chunk[ch], b.s_rng)) != cudaSuccess) return e;
+            if ((e = cudaEventRecord(b.ev_chunk[nxt], b.s_rng)) != cudaSuccess) return e;
         }
-        const int r0 = ch * Mc;
-        const uint8_t* ao = static_cast<const uint8_t*>(x.attn_in ? x.attn_in : x.attn_o) + static_cast<uint64_t>(r0) * d * 2;
-        uint8_t* ao8 = static_cast<uint8_t*>(x.attn_o8) + static_cast<uint64_t>(r0) * d;
-        if ((e = launch_quant_e4m3(ao, ao8, static_cast<uint64_t>(Mc) * d, c.s_attn, s)) != cudaSuccess) return e;
+        RngQueue q = queue_for(nxt);
+        const RngQueue* rq = b.mode == BLOCK_IN_GEMM ? &q : nullptr;
+        // stage ch's GEMMs on window ch's rows: blocks of Sc rows every S rows from row r0
+        auto rows = [&](GemmJob& g) {
+            g.rb = Sc; g.rstride = S; g.roff = r0; g.a_rows = M;
+            g.pdl = chunk_pdl();
+            g.rng = rq;
+            g.rng_warps = rw;
+        };
+        if ((e = launch_quant_e4m3_rows(x.attn_o, x.attn_o8, Mc, d, Sc, S, r0, c.s_attn, s)) != cudaSuccess) return e;
         ++n;
         GemmJob g;
-        g = gemm(c, Mc, d, d, ao8, x.wo, const_cast<uint8_t*>(rows8(x.y1, r0, d)), rgo_gk::EPI_NONE, rgo_gk::OUT_E4M3,
-                 c.a_proj, c.s_proj);
-        g.pdl = false;  // chunked: event joins between streams; kept on plain stream order
+        g = gemm(c, Mc, d, d, x.attn_o8, x.wo, x.y1, rgo_gk::EPI_NONE, rgo_gk::OUT_E4M3, c.a_proj, c.s_proj);
+        rows(g);
         if ((e = launch_gemm(g, s)) != cudaSuccess) return e;
         ++n;
-        g = gemm(c, Mc, n1, d, rows8(x.y1, r0, d), x.w1, const_cast<uint8_t*>(rows8(x.h, r0, F)),
-                 c.gated ? rgo_gk::EPI_SWIGLU : rgo_gk::EPI_GELU, rgo_gk::OUT_E4M3, c.a_ffn1, c.s_ffn1);
-        g.pdl = false;  // chunked: event joins between streams; kept on plain stream order
+        g = gemm(c, Mc, n1, d, x.y1, x.w1, x.h, c.gated ? rgo_gk::EPI_SWIGLU : rgo_gk::EPI_GELU, rgo_gk::OUT_E4M3,
+                 c.a_ffn1, c.s_ffn1);
+        rows(g);
         if ((e = launch_gemm(g, s)) != cudaSuccess) return e;
         ++n;
-        g = gemm(c, Mc, d, F, rows8(x.h, r0, F), x.w2, const_cast<uint8_t*>(rows8(x.x, r0, d)), rgo_gk::EPI_NONE,
-                 rgo_gk::OUT_E4M3, c.a_ffn2, c.s_ffn2);
-        g.pdl = false;  // chunked: event joins between streams; kept on plain stream order
+        g = gemm(c, Mc, d, F, x.h, x.w2, x.x, rgo_gk::EPI_NONE, rgo_gk::OUT_E4M3, c.a_ffn2, c.s_ffn2);
+        rows(g);
         if ((e = launch_gemm(g, s)) != cudaSuccess) return e;
         ++n;
-        void* qkv_c = static_cast<uint8_t*>(x.qkv) + static_cast<uint64_t>(r0) * 3 * d * 2;
-        g = gemm(c, Mc, 3 * d, d, rows8(x.x, r0, d), x.wqkv, qkv_c, rgo_gk::EPI_NONE, rgo_gk::OUT_BF16, c.a_qkv, 1.0f);
-        g.pdl = false;  // chunked: event joins between streams; kept on plain stream order
+        g = gemm(c, Mc, 3 * d, d, x.x, x.wqkv, x.qkv_out, rgo_gk::EPI_NONE, rgo_gk::OUT_BF16, c.a_qkv, 1.0f);
+        rows(g);
         if ((e = launch_gemm(g, s)) != cudaSuccess) return e;
         ++n;
-        if (ch == C - 1 && (e = record_timing(b, 1, s)) != cudaSuccess) return e;
-        if (b.mode == BLOCK_STREAMS && (e = cudaStreamWaitEvent(s, b.ev_chunk[ch], 0)) != cudaSuccess) return e;
-        if (ch == C - 1 && (e = record_timing(b, 3, s)) != cudaSuccess) return e;
-        AttnJob a{};
-        a.B = Bc; a.H = c.heads; a.S = c.seq; a.HD = c.head_dim;
-        a.scale = 1.0f / sqrtf(static_cast<float>(c.head_dim));
-        const long long ld = 3LL * d;
-        const __nv_bfloat16* qkv = static_cast<const __nv_bfloat16*>(qkv_c);
-        a.q = {qkv, static_cast<long long>(c.seq) * ld, c.head_dim, ld};
-        a.k = {qkv + d, static_cast<long long>(c.seq) * ld, c.head_dim, ld};
-        a.v = {qkv + 2 * d, static_cast<long long>(c.seq) * ld, c.head_dim, ld};
-        a.o = {static_cast<uint8_t*>(x.attn_o) + static_cast<uint64_t>(r0) * d * 2, static_cast<long long>(c.seq) * d,
-               c.head_dim, d};
-        a.lse = x.lse ? x.lse + static_cast<uint64_t>(ch) * Bc * c.heads * c.seq : nullptr;
-        a.mode = b.mode == BLOCK_SERIAL_FUSED ? rgo_attn::MASK_PHILOX : rgo_attn::MASK_BITS;
-        a.keep_prob = c.keep_prob;
-        a.bits = bits;
-        a.bits_bytes = chunk_bytes;
-        a.seed = c.seed;
-        a.base_offset = base;
-        a.threshold = c.threshold;
-        a.rounds = c.rounds;
-        if ((e = launch_attn_fwd(a, s)) != cudaSuccess) return e;
-        ++n;
-        if (b.mode == BLOCK_STREAMS && (e = cudaEventRecord(b.ev_slot[ch], s)) != cudaSuccess) return e;
+        if (b.mode == BLOCK_IN_GEMM) {  // what the stage's RNG warps left of window nxt
+            if ((e = launch_rng_queue(q, 0, 0, 0, s, chunk_pdl())) != cudaSuccess) return e;
+            ++n;
+        }
     }
-    if (b.mode == BLOCK_STREAMS && (e = cudaStreamWaitEvent(s, b.ev_chunk[C - 1], 0)) != cudaSuccess) return e;
+    // join: window 0's mask for the next step is complete when the step ends
+    if (b.mode == BLOCK_STREAMS && (e = cudaStreamWaitEvent(s, b.ev_chunk[0], 0)) != cudaSuccess) return e;
+    // phase split is not meaningful across interleaved stages: [GEMM window] = the whole step
+    if ((e = record_timing(b, 1, s)) != cudaSuccess) return e;
+    if ((e = record_timing(b, 3, s)) != cudaSuccess) return e;
     if ((e = record_timing(b, 2, s)) != cudaSuccess) return e;
     *launches = n;
+    return cudaSuccess;
+}
+
+// First chunked step: the mask of window 0 (generated by the previous step's last
+// stage in steady state) -- and for NO_RNG, which never generates, windows 0 and 1.
+static cudaError_t prime_chunked(Block& b, cudaStream_t s) {
+    const BlockConfig& c = b.cfg;
+    const int C = c.chunks, S = c.seq, Sc = S / C;
+    const uint64_t win_elems = static_cast<uint64_t>(c.batch) * c.heads * Sc * static_cast<uint64_t>(S);
+    const int wins = b.mode == BLOCK_NO_RNG ? 2 : (b.mode == BLOCK_SERIAL_FUSED ? 0 : 1);
+    for (int w = 0; w < wins; ++w) {
+        MaskJob mj{b.buf.mask + w * (win_elems / 8), win_elems, c.seed, c.base_offset, c.threshold, c.rounds};
+        mj.win_rows = static_cast<uint32_t>(Sc);
+        mj.row0 = static_cast<uint32_t>(w * Sc);
+        mj.seq = static_cast<uint32_t>(S);
+        if (cudaError_t e = launch_mask(mj, LaunchShape{}, s); e != cudaSuccess) return e;
+    }
     return cudaSuccess;
 }
 
@@ -490,6 +585,10 @@ cudaError_t block_step(Block* b, cudaStream_t stream, int* launches) {
     if ((e = cudaEventRecord(b->ev_in, stream)) != cudaSuccess) return e;
     if ((e = cudaStreamWaitEvent(b->s_main, b->ev_in, 0)) != cudaSuccess) return e;
     int n = 0;
+    if (b->cfg.chunks > 1 && !b->primed) {
+        if ((e = prime_chunked(*b, b->s_main)) != cudaSuccess) return e;
+        b->primed = true;
+    }
     if (b->exec) {
         e = cudaGraphLaunch(b->exec, b->s_main);
         n = b->launches_per_step;

@@ -23,9 +23,11 @@ struct BlockConfig {
     // MoE FFN (experts > 0): `experts` expert FFNs of width ffn, top_k experts
     // per token, balanced synthetic routing (see moe_slot)
     int experts, top_k;
-    // SQ/batch-chunk pipelining (schedule.hpp:206-239): chunks > 1 splits the
-    // batch into `chunks` groups; each group's GEMMs, mask and attention form
-    // one pipeline stage and the live mask is a 2-slot ring of chunk masks
+    // SQ-chunk pipelining (schedule.hpp:205-239): chunks > 1 splits the query
+    // rows of every sequence into `chunks` windows of seq/chunks rows; the step
+    // becomes C stages [attention(c) -> Proj/FFN/QKV of window c] with the RNG
+    // of window c+1 hidden under stage c's GEMMs, and the live mask is a 2-slot
+    // ring of window masks (2/C of the full mask)
     int chunks;
 };
 
@@ -48,6 +50,8 @@ struct BlockBuffers {
     void* ye;       // MoE: bf16 [M*top_k, d] expert FFN outputs before the combine
     const void* attn_in;  // bf16 [M, d] step input (previous block's attention output);
                           // null: attn_o, i.e. each step consumes the previous step's output
+    void* qkv_out;  // chunked: bf16 [M, 3d] the step's QKV GEMM output (the step's attention
+                    // reads qkv, written by the previous step); counter then has chunks entries
 };
 
 struct Block;
@@ -60,5 +64,8 @@ cudaError_t block_last_timings(Block* b, float* ms2);
 cudaError_t block_last_timings3(Block* b, float* ms3);
 void block_destroy(Block* b);
 cudaError_t launch_quant_e4m3(const void* in, void* out, uint64_t n, float scale, cudaStream_t s);
+// Rows r < rows of [*, d] bf16 -> e4m3, row r at (r / rb) * rstride + roff + r % rb.
+cudaError_t launch_quant_e4m3_rows(const void* in, void* out, int rows, int d, int rb, int rstride, int roff,
+                                   float scale, cudaStream_t s);
 
 }  // namespace rgo

@@ -490,10 +490,13 @@ int rgo_block_create(const rgo_block_desc* d, const rgo_block_buffers* b, int32_
         if (!b->xd || !b->ye) return fail(RGO_EINVAL, "rgo_block_create: MoE needs the xd and ye buffers");
     }
     const uint32_t chunks = d->chunks > 1 ? d->chunks : 1;
-    if (chunks > 1 && (d->batch % chunks || d->experts || mode == RGO_OVERLAP_IN_GEMM))
-        return fail(RGO_EINVAL, "rgo_block_create: chunks must divide batch (dense FFN, not IN_GEMM)");
+    if (chunks > 1 && (d->seq % chunks || (d->seq / chunks) % 128 || d->experts))
+        return fail(RGO_EINVAL, "pipeline_schedule: chunks must divide SQ (into windows of a multiple of 128 rows; "
+                                "dense FFN)");
+    if (chunks > 64) return fail(RGO_EINVAL, "rgo_block_create: at most 64 chunks");
+    if (chunks > 1 && !b->qkv_out) return fail(RGO_EINVAL, "rgo_block_create: chunked step needs qkv_out");
     const uint64_t n_full = static_cast<uint64_t>(d->batch) * d->heads * d->seq * static_cast<uint64_t>(d->seq);
-    const uint64_t n = chunks > 1 ? 2 * (n_full / chunks) : n_full;  // chunked: 2-slot ring
+    const uint64_t n = chunks > 1 ? 2 * (n_full / chunks) : n_full;  // chunked: 2-slot ring of window masks
     if (!b->mask || b->mask_bytes < n / 8 || !b->counter || !b->x || !b->wqkv || !b->wo || !b->w1 || !b->w2 ||
         !b->qkv || !b->attn_o || !b->attn_o8 || !b->y1 || !b->h)
         return fail(RGO_EINVAL, "rgo_block_create: missing buffer (mask needs %llu bytes)",
@@ -515,7 +518,7 @@ int rgo_block_create(const rgo_block_desc* d, const rgo_block_buffers* b, int32_
     c.top_k = static_cast<int>(d->top_k);
     c.chunks = static_cast<int>(chunks);
     rgo::BlockBuffers bb{b->x, b->wqkv, b->wo, b->w1, b->w2, b->qkv, b->attn_o, b->attn_o8, b->y1, b->h,
-                         b->mask, b->mask_bytes, b->counter, b->lse, b->xd, b->ye, b->attn_in};
+                         b->mask, b->mask_bytes, b->counter, b->lse, b->xd, b->ye, b->attn_in, b->qkv_out};
     rgo::Block* impl = nullptr;
     cudaError_t ce = rgo::block_create(c, bb, mode, d->use_graph != 0, &impl);
     if (ce != cudaSuccess) return cuda_fail(ce, "rgo_block_create");

@@ -4,6 +4,8 @@
 
 #include <cstdint>
 
+#include "rgo_internal.h"
+
 namespace rgo_gk {
 enum { EPI_NONE = 0, EPI_SWIGLU = 1, EPI_GELU = 2 };
 enum { OUT_BF16 = 0, OUT_E4M3 = 1 };
@@ -23,6 +25,7 @@ struct RngQueue {
     uint32_t k0, k1, thr;    // key, threshold (< 2^32)
     int rounds;
     unsigned long long* counter;
+    VecWindow win;           // row window of the layout (chunked pipeline); wv == 0: whole layout
 };
 
 struct GemmJob {
@@ -43,6 +46,11 @@ struct GemmJob {
     const RngQueue* rng;     // non-null: co-resident RNG warps drain this queue
     int rng_warps;           // 4, 6, 8, 12 or 16 (0 = RNG_WARPS_IN_GEMM; the block picks per workload)
     bool pdl;                // programmatic dependent launch after the previous kernel in the stream
+    // Row blocks (SQ-chunk pipelining): when rb > 0, GEMM row r (< M) is row
+    // (r / rb) * rstride + roff + r % rb of A and C (rb % 128 == 0), and A's
+    // tensor map spans a_rows rows.  rb == 0: rows are contiguous.
+    int rb, rstride, roff, a_rows;
+    int group_m;             // M-blocks (256 rows) per rasterisation group; 0 = default
 };
 
 cudaError_t launch_gemm(const GemmJob& j, cudaStream_t s);

@@ -28,6 +28,8 @@
 //   core runs, using the registers TMEM frees.
 #include "gemm_sm100.cuh"
 
+#include <cstdlib>
+
 namespace rgo_gk {  // instantiated in gemm_inst_*.cu
 RGO_GEMM_EXTERN(true, EPI_NONE, OUT_BF16)
 RGO_GEMM_EXTERN(true, EPI_NONE, OUT_E4M3)
@@ -50,8 +52,9 @@ cudaError_t launch_gemm(const GemmJob& j, cudaStream_t s) {
     if (j.epi == EPI_SWIGLU && j.N % BN != 0) return cudaErrorInvalidValue;
     const CUtensorMapDataType dt = fp8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
     CUtensorMap ta, tb;
+    if (j.rb && (j.rb % BM || j.M % j.rb || j.a_rows <= 0)) return cudaErrorInvalidValue;
     {
-        const uint64_t dims[2] = {static_cast<uint64_t>(j.K), static_cast<uint64_t>(j.M)};
+        const uint64_t dims[2] = {static_cast<uint64_t>(j.K), static_cast<uint64_t>(j.rb ? j.a_rows : j.M)};
         const uint64_t strides[1] = {static_cast<uint64_t>(j.lda) * esz};
         const uint32_t box[2] = {static_cast<uint32_t>(BKB / esz), BM};
         if (!make_tmap(&ta, j.A, dt, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B))
@@ -76,6 +79,18 @@ cudaError_t launch_gemm(const GemmJob& j, cudaStream_t s) {
     p.alpha = j.alpha;
     p.out_scale = j.out_scale;
     p.pdl = j.pdl ? 1 : 0;
+    // Rasterisation group (M-blocks swept together over all N-blocks): the
+    // group's A rows stay in L2 while B streams through once per group, so the
+    // DRAM reads are A + B * ceil(tiles_m / group_m).  RGO_GEMM_GROUP_M overrides
+    // (measurement A/B); 0 = the default.
+    static const int group_env = [] {
+        const char* e = getenv("RGO_GEMM_GROUP_M");
+        return e ? atoi(e) : 0;
+    }();
+    p.group_m = j.group_m > 0 ? j.group_m : (group_env > 0 ? group_env : GROUP_M);
+    p.rb = j.rb;
+    p.rstride = j.rstride;
+    p.roff = j.roff;
     if (j.rng) p.rng = *j.rng;
     const int tiles = p.tiles_m * p.tiles_n;
     int grid = j.grid > 0 ? j.grid : num_sms();

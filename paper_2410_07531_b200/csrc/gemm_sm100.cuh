@@ -42,13 +42,21 @@ struct Params {
     // co-resident RNG (mechanism B)
     rgo::RngQueue rng;
     int pdl;              // launched as a programmatic dependent of the previous kernel
+    int rb, rstride, roff;  // row blocks (GemmJob::rb): GEMM row r -> A/C row map_row(r)
+    int group_m;            // M-blocks per rasterisation group
 };
 
-__device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, int& mb, int& nb) {
-    const int per_group = GROUP_M * tiles_n;
+// GEMM row -> row of A and C: contiguous, or blocks of rb rows every rstride
+// rows starting at roff (the query-row chunk of every batch item).
+__device__ __forceinline__ int map_row(const Params& p, int r) {
+    return p.rb ? (r / p.rb) * p.rstride + p.roff + r % p.rb : r;
+}
+
+__device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, int group_m, int& mb, int& nb) {
+    const int per_group = group_m * tiles_n;
     const int group = tile / per_group;
-    const int first_m = group * GROUP_M;
-    const int gsize = min(tiles_m - first_m, GROUP_M);
+    const int first_m = group * group_m;
+    const int gsize = min(tiles_m - first_m, group_m);
     const int local = tile - group * per_group;
     mb = first_m + local % gsize;
     nb = local / gsize;
@@ -161,8 +169,8 @@ __global__ void __launch_bounds__(CORE_THREADS + 32 * RNG_WARPS, 1)
         const uint32_t sa = smem_u32(smA), sb = smem_u32(smB), eb0 = smem_u32(&empty[0]);
         for (int tile = pair; tile < num_tiles; tile += n_pairs) {
             int mb, nb;
-            tile_coords(tile, p.tiles_m, p.tiles_n, mb, nb);
-            const int row_a = mb * TILE_M + rank * BM, row_b = nb * BN + rank * (BN / 2);
+            tile_coords(tile, p.tiles_m, p.tiles_n, p.group_m, mb, nb);
+            const int row_a = map_row(p, mb * TILE_M + rank * BM), row_b = nb * BN + rank * (BN / 2);
             for (int kb = 0; kb < kblocks; ++kb) {
                 mbar_wait(eb0 + 8 * stage, phase ^ 1);
                 if (elect_one()) {
@@ -224,10 +232,11 @@ __global__ void __launch_bounds__(CORE_THREADS + 32 * RNG_WARPS, 1)
         uint32_t acc = 0, acc_phase = 0;
         for (int tile = pair; tile < num_tiles; tile += n_pairs) {
             int mb, nb;
-            tile_coords(tile, p.tiles_m, p.tiles_n, mb, nb);
+            tile_coords(tile, p.tiles_m, p.tiles_n, p.group_m, mb, nb);
             mbar_wait(smem_u32(&tfull[acc]), acc_phase);
             tc_fence_after();
-            const int row = mb * TILE_M + row_in_tile;
+            const int row_l = mb * TILE_M + row_in_tile;
+            const int row = map_row(p, row_l);
             const uint32_t tbase = tmem_base + ((q * 32) << 16) + acc * BN;
             if constexpr (EPI == EPI_SWIGLU) {
 #pragma unroll 1
@@ -243,7 +252,7 @@ __global__ void __launch_bounds__(CORE_THREADS + 32 * RNG_WARPS, 1)
                         v[i] = silu(__uint_as_float(g[i]) * p.alpha) * (__uint_as_float(u[i]) * p.alpha) *
                                p.out_scale;
                     const int col = nb * (BN / 2) + c * 32;
-                    if (row < p.M && col < p.n_out) store32<OUT>(p.C, p.ldc, row, col, v);
+                    if (row_l < p.M && col < p.n_out) store32<OUT>(p.C, p.ldc, row, col, v);
                 }
             } else {
 #pragma unroll 1
@@ -259,7 +268,7 @@ __global__ void __launch_bounds__(CORE_THREADS + 32 * RNG_WARPS, 1)
                         v[i] = x * p.out_scale;
                     }
                     const int col = nb * BN + c * 32;
-                    if (row < p.M && col < p.n_out) store32<OUT>(p.C, p.ldc, row, col, v);
+                    if (row_l < p.M && col < p.n_out) store32<OUT>(p.C, p.ldc, row, col, v);
                 }
             }
             tc_fence_before();

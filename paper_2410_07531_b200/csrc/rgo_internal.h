@@ -25,7 +25,35 @@ struct MaskJob {
     uint64_t base_offset;
     uint64_t threshold;     // KeepThreshold::threshold(), in [0, 2^32]
     int rounds;             // [1,16]
+    // Row window (SQ-chunk pipelining, schedule.hpp:205-239): when win_rows > 0,
+    // `elems` = slices * win_rows * seq and out holds the compact chunk mask
+    // [slice][win_rows][seq] of rows [row0, row0 + win_rows) of every slice of a
+    // layout with `seq` rows/keys: element (s, i, j) takes the keep bit of the
+    // full layout's element (s*seq + row0 + i)*seq + j.  Needs seq % 128 == 0.
+    uint32_t win_rows = 0, row0 = 0, seq = 0;
 };
+
+// Vector (128-element unit) index map of a row window: compact chunk vector v ->
+// vector of the full layout.  wv = vectors per slice window, sv = per slice,
+// ov = vector offset of the window's first row.  wv == 0: identity.
+struct VecWindow {
+    uint64_t wv = 0, sv = 0, ov = 0;
+};
+__host__ __device__ inline uint64_t window_vec(const VecWindow& w, uint64_t v) {
+    if (w.wv == 0) return v;
+    const uint64_t s = v < 0xFFFFFFFFull && w.wv <= 0xFFFFFFFFull
+                           ? static_cast<uint64_t>(static_cast<uint32_t>(v) / static_cast<uint32_t>(w.wv))
+                           : v / w.wv;
+    return s * w.sv + w.ov + (v - s * w.wv);
+}
+inline VecWindow make_window(uint32_t win_rows, uint32_t row0, uint32_t seq) {
+    VecWindow w;
+    if (win_rows == 0) return w;
+    w.wv = static_cast<uint64_t>(win_rows) * seq / 128;
+    w.sv = static_cast<uint64_t>(seq) * seq / 128;
+    w.ov = static_cast<uint64_t>(row0) * seq / 128;
+    return w;
+}
 
 // Kernel attributes are per device: set the dynamic shared-memory opt-in once
 // per (kernel, current device), so launches on a second GPU of the same

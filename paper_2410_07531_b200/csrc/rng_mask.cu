@@ -30,18 +30,20 @@ __device__ __forceinline__ void st_v4_streaming(uint8_t* p, uint32_t a, uint32_t
                  : "memory");
 }
 
-// Vectors [0, n_vec) of the mask; vector v covers elements [128v, 128v+128).
-template <int R>
+// Vectors [0, n_vec) of the mask; vector v covers elements [128v, 128v+128)
+// (WIN: of the row window `win`, written compactly; counters of the full layout).
+template <int R, bool WIN>
 __global__ void __launch_bounds__(256, (R == 4 || R == 5) ? 4 : 0) rng_mask_kernel(uint8_t* __restrict__ out, uint64_t n_vec,
                                                        uint64_t base_offset, uint32_t k0,
-                                                       uint32_t k1, uint32_t thr, uint32_t zero) {
+                                                       uint32_t k1, uint32_t thr, uint32_t zero,
+                                                       const rgo::VecWindow win) {
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
     // key / threshold in vector registers rather than uniform registers, so a
     // co-resident GEMM keeps the uniform datapath it issues MMAs/TMA through
     asm volatile("" : "+r"(k0), "+r"(k1), "+r"(thr) : "r"(threadIdx.x));
     for (uint64_t v = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < n_vec;
          v += stride) {
-        const uint64_t ctr = base_offset + v * 32;  // 64-bit wrap like element_source
+        const uint64_t ctr = base_offset + (WIN ? rgo::window_vec(win, v) : v) * 32;  // 64-bit wrap like element_source
         const uint32_t lo = static_cast<uint32_t>(ctr), hi = static_cast<uint32_t>(ctr >> 32);
         uint32_t w0, w1, w2, w3;
         if (lo <= 0xFFFFFFFFu - 31u) {  // no carry into c1 inside this unit
@@ -113,10 +115,13 @@ static void prefer_max_smem(K kernel) {
 
 template <int R>
 static cudaError_t launch_r(uint8_t* out, uint64_t n_vec, uint64_t base, uint32_t k0, uint32_t k1,
-                            uint32_t thr, const rgo::LaunchShape& ls, cudaStream_t s) {
-    static bool once = (prefer_max_smem(rng_mask_kernel<R>), true);
+                            uint32_t thr, const rgo::LaunchShape& ls, const rgo::VecWindow& win, cudaStream_t s) {
+    static bool once = (prefer_max_smem(rng_mask_kernel<R, false>), prefer_max_smem(rng_mask_kernel<R, true>), true);
     (void)once;
-    rng_mask_kernel<R><<<ls.grid, ls.block, ls.dyn_smem, s>>>(out, n_vec, base, k0, k1, thr, 0u);
+    if (win.wv)
+        rng_mask_kernel<R, true><<<ls.grid, ls.block, ls.dyn_smem, s>>>(out, n_vec, base, k0, k1, thr, 0u, win);
+    else
+        rng_mask_kernel<R, false><<<ls.grid, ls.block, ls.dyn_smem, s>>>(out, n_vec, base, k0, k1, thr, 0u, win);
     return cudaGetLastError();
 }
 
@@ -124,7 +129,21 @@ static const void* kernel_ptr(int rounds) {
     switch (rounds) {
 #define RGO_CASE(R) \
     case R:         \
-        return reinterpret_cast<const void*>(&rng_mask_kernel<R>);
+        return reinterpret_cast<const void*>(&rng_mask_kernel<R, false>);
+        RGO_CASE(1) RGO_CASE(2) RGO_CASE(3) RGO_CASE(4) RGO_CASE(5) RGO_CASE(6) RGO_CASE(7)
+        RGO_CASE(8) RGO_CASE(9) RGO_CASE(10) RGO_CASE(11) RGO_CASE(12) RGO_CASE(13)
+        RGO_CASE(14) RGO_CASE(15) RGO_CASE(16)
+#undef RGO_CASE
+        default:
+            return nullptr;
+    }
+}
+
+static const void* kernel_ptr_win(int rounds) {
+    switch (rounds) {
+#define RGO_CASE(R) \
+    case R:         \
+        return reinterpret_cast<const void*>(&rng_mask_kernel<R, true>);
         RGO_CASE(1) RGO_CASE(2) RGO_CASE(3) RGO_CASE(4) RGO_CASE(5) RGO_CASE(6) RGO_CASE(7)
         RGO_CASE(8) RGO_CASE(9) RGO_CASE(10) RGO_CASE(11) RGO_CASE(12) RGO_CASE(13)
         RGO_CASE(14) RGO_CASE(15) RGO_CASE(16)
@@ -166,6 +185,8 @@ cudaError_t launch_mask(const MaskJob& j, const LaunchShape& shape_in, cudaStrea
     }
     const uint32_t thr = static_cast<uint32_t>(j.threshold);
     const uint64_t n_vec = n / 128;
+    const VecWindow win = make_window(j.win_rows, j.row0, j.seq);
+    if (j.win_rows && (j.seq % 128 || n % 128)) return cudaErrorInvalidValue;
     if (n_vec > 0) {
         LaunchShape ls = shape_in;
         if (ls.block == 0) ls.block = 256;
@@ -176,14 +197,17 @@ cudaError_t launch_mask(const MaskJob& j, const LaunchShape& shape_in, cudaStrea
             const uint64_t cap = static_cast<uint64_t>(num_sms()) * occ;
             ls.grid = static_cast<unsigned>(want < cap ? want : cap);
         }
-        if (ls.dyn_smem > 48 * 1024)
+        if (ls.dyn_smem > 48 * 1024) {
             cudaFuncSetAttribute(kernel_ptr(j.rounds), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(ls.dyn_smem));
+            cudaFuncSetAttribute(kernel_ptr_win(j.rounds), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(ls.dyn_smem));
+        }
         cudaError_t e;
         switch (j.rounds) {
 #define RGO_CASE(R)                                                     \
     case R:                                                             \
-        e = launch_r<R>(j.out, n_vec, j.base_offset, k0, k1, thr, ls, s); \
+        e = launch_r<R>(j.out, n_vec, j.base_offset, k0, k1, thr, ls, win, s); \
         break;
             RGO_CASE(1) RGO_CASE(2) RGO_CASE(3) RGO_CASE(4) RGO_CASE(5) RGO_CASE(6) RGO_CASE(7)
             RGO_CASE(8) RGO_CASE(9) RGO_CASE(10) RGO_CASE(11) RGO_CASE(12) RGO_CASE(13)

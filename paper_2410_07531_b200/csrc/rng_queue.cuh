@@ -3,7 +3,8 @@
 // global counter; the same device routine runs inside the GEMM CTAs
 // (co-resident RNG warps, until the GEMM's epilogue warps finish) and in the
 // tail kernel that drains whatever the GEMMs left.  Bits are identical to K1:
-// vector v = elements [128v, 128v+128), counter base + 32v.
+// vector v = elements [128v, 128v+128), counter base + 32v (of the full
+// layout's vector window_vec(win, v) when the queue covers a row window).
 #pragma once
 #include <cstdint>
 
@@ -15,7 +16,7 @@ namespace rgo {
 // k0/k1/thr arrive as per-thread (vector-register) copies: see rng_drain_r.
 template <int R>
 __device__ __forceinline__ void rng_vector(const RngQueue& q, uint64_t v, uint32_t k0, uint32_t k1, uint32_t thr) {
-    const uint64_t ctr = q.base_offset + v * 32;
+    const uint64_t ctr = q.base_offset + window_vec(q.win, v) * 32;
     const uint32_t lo = static_cast<uint32_t>(ctr), hi = static_cast<uint32_t>(ctr >> 32);
     uint32_t w0, w1, w2, w3;
     if (lo <= 0xFFFFFFFFu - 31u) {
@@ -38,7 +39,7 @@ __device__ __forceinline__ void rng_vector(const RngQueue& q, uint64_t v, uint32
 template <int R>
 __device__ __forceinline__ void rng_vector2(const RngQueue& q, uint64_t va, uint64_t vb, uint32_t k0, uint32_t k1,
                                             uint32_t thr) {
-    const uint64_t ca = q.base_offset + va * 32, cb = q.base_offset + vb * 32;
+    const uint64_t ca = q.base_offset + window_vec(q.win, va) * 32, cb = q.base_offset + window_vec(q.win, vb) * 32;
     const uint32_t la = static_cast<uint32_t>(ca), lb = static_cast<uint32_t>(cb);
     if (la > 0xFFFFFFFFu - 31u || lb > 0xFFFFFFFFu - 31u) {  // rare: a unit straddles a 2^32 counter boundary
         rng_vector<R>(q, va, k0, k1, thr);
@@ -98,7 +99,7 @@ __device__ __forceinline__ void rng_drain_rt(const RngQueue& q, const volatile i
         if (start >= q.n_vec) break;
         const uint64_t v = start + lane;
         if (v < q.n_vec) {
-            const uint64_t ctr = q.base_offset + v * 32;
+            const uint64_t ctr = q.base_offset + window_vec(q.win, v) * 32;
             uint32_t w[4];
 #pragma unroll 1
             for (int t = 0; t < 4; ++t) w[t] = rgo_dev::keep32_rt(ctr + 8 * t, q.k0, q.k1, q.thr, q.rounds);

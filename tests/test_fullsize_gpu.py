@@ -144,3 +144,16 @@ def test_attention_bwd_sq4096(rgo, cuda):
     want = oracle.attention_backward(np64(q), np64(k), np64(v), np64(do), B * H, S, D, keep, 0.9)
     errs = [rel(np64(x).reshape(B * H, S, D), w) for x, w in zip((o, dq, dk, dv), want)]
     assert max(errs) <= TOL_BF16, errs
+
+
+def test_seq32k_chunked_pipeline(rgo, cuda):
+    """Config S at its longest point (B1 nH32 SQ32K, Llama2 head config): the
+    SQ-chunk pipeline with C = 8 windows (live mask 2 x 512 MiB instead of
+    4 GiB, schedule.hpp:205-239 / capacity.hpp:51-59) equals the unchunked step
+    bitwise in the in-GEMM mode."""
+    import sys
+    sys.path.insert(0, __file__.rsplit("/", 1)[0])
+    from test_block_gpu import chunked_vs_unchunked
+    cfg = rgo.WorkloadConfig(batch=1, seq=32768, heads=32, head_dim=128, ffn_dim=11008, gated=True, keep_prob=0.9,
+                             philox_rounds=10)
+    chunked_vs_unchunked(rgo, cfg, "in_gemm", 8, seed=42)
