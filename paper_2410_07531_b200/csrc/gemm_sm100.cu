@@ -28,6 +28,7 @@
 //   core runs, using the registers TMEM frees.
 #include "gemm_sm100.cuh"
 
+#include <algorithm>
 #include <cstdlib>
 
 namespace rgo_gk {  // instantiated in gemm_inst_*.cu
@@ -87,7 +88,13 @@ cudaError_t launch_gemm(const GemmJob& j, cudaStream_t s) {
         const char* e = getenv("RGO_GEMM_GROUP_M");
         return e ? atoi(e) : 0;
     }();
-    p.group_m = j.group_m > 0 ? j.group_m : (group_env > 0 ? group_env : GROUP_M);
+    // Default: as many M-blocks as fit ~32 MB of A (256 rows x K per block) --
+    // the measured optimum (scripts/diag/gemm_group_sweep.py, profiles/r02_gemm_raster.md):
+    // at Llama2-7B FFN1 DRAM reads 455 -> 290 MB per launch and 0.929 -> 0.910 ms,
+    // QKV 283 -> 226 MB and 0.564 -> 0.555 ms; 64 blocks (64 MB) thrash L2 (1 GB).
+    const int auto_group = static_cast<int>(
+        std::max<long long>(1, std::min<long long>(64, (32ll << 20) / (static_cast<long long>(TILE_M) * j.K * esz))));
+    p.group_m = j.group_m > 0 ? j.group_m : (group_env > 0 ? group_env : auto_group);
     p.rb = j.rb;
     p.rstride = j.rstride;
     p.roff = j.roff;
