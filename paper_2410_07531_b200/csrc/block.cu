@@ -209,6 +209,14 @@ static bool chunk_pdl() {
     return on && block_pdl();
 }
 
+static int rng_gemms_attach() {
+    static const int n = [] {
+        const char* e = getenv("RGO_RNG_GEMMS");
+        return e ? atoi(e) : 0;
+    }();
+    return n;
+}
+
 static GemmJob gemm(const BlockConfig& c, int M, int N, int K, const void* A, const void* B, void* C, int epi,
                     int out, float alpha, float out_scale) {
     GemmJob j{};
@@ -292,7 +300,13 @@ static cudaError_t enqueue_step(Block& b, int* launches) {
     } else if (b.mode == BLOCK_IN_GEMM) {
         if ((e = cudaMemsetAsync(x.counter, 0, sizeof(unsigned long long), s)) != cudaSuccess) return e;
     }
-    const RngQueue* rq = b.mode == BLOCK_IN_GEMM ? &q : nullptr;
+    const RngQueue* rq_all = b.mode == BLOCK_IN_GEMM ? &q : nullptr;
+    // IN_GEMM: the first `rng_gemms` GEMMs of the step carry RNG warps (0 = all;
+    // RGO_RNG_GEMMS overrides): with little mask per GEMM flop the queue empties
+    // inside the first GEMMs and later GEMMs need not pay for idle RNG warps
+    const int attach = rng_gemms_attach();
+    int gemm_idx = 0;
+    auto rq_next = [&]() -> const RngQueue* { return (attach == 0 || gemm_idx++ < attach) ? rq_all : nullptr; };
     if ((e = record_timing(b, 0, s)) != cudaSuccess) return e;
     // attention output of the previous block -> e4m3
     if ((e = launch_quant_e4m3(x.attn_in ? x.attn_in : x.attn_o, x.attn_o8, static_cast<uint64_t>(M) * d, c.s_attn,
@@ -301,7 +315,7 @@ static cudaError_t enqueue_step(Block& b, int* launches) {
     ++n;
     GemmJob g;
     g = gemm(c, M, d, d, x.attn_o8, x.wo, x.y1, rgo_gk::EPI_NONE, rgo_gk::OUT_E4M3, c.a_proj, c.s_proj);
-    g.rng = rq;
+    g.rng = rq_next();
     // IN_GEMM: RNG warps per GEMM CTA (4, 6, 8, 12 or 16; 0 = auto_rng_warps)
     const int rw = c.rng_block ? static_cast<int>(c.rng_block) : auto_rng_warps(c);
     g.rng_warps = rw;
@@ -318,14 +332,14 @@ static cudaError_t enqueue_step(Block& b, int* launches) {
             uint8_t* h = static_cast<uint8_t*>(x.h) + static_cast<uint64_t>(ex) * me * F;
             g = gemm(c, me, n1, d, xd, static_cast<const uint8_t*>(x.w1) + static_cast<uint64_t>(ex) * n1 * d, h,
                      c.gated ? rgo_gk::EPI_SWIGLU : rgo_gk::EPI_GELU, rgo_gk::OUT_E4M3, c.a_ffn1, c.s_ffn1);
-            g.rng = rq;
+            g.rng = rq_next();
             g.rng_warps = rw;
             if ((e = launch_gemm(g, s)) != cudaSuccess) return e;
             ++n;
             g = gemm(c, me, d, F, h, static_cast<const uint8_t*>(x.w2) + static_cast<uint64_t>(ex) * d * F,
                      static_cast<__nv_bfloat16*>(x.ye) + static_cast<uint64_t>(ex) * me * d, rgo_gk::EPI_NONE,
                      rgo_gk::OUT_BF16, c.a_ffn2, c.s_ffn2);
-            g.rng = rq;
+            g.rng = rq_next();
             g.rng_warps = rw;
             if ((e = launch_gemm(g, s)) != cudaSuccess) return e;
             ++n;
@@ -337,18 +351,18 @@ static cudaError_t enqueue_step(Block& b, int* launches) {
     } else {
         g = gemm(c, M, n1, d, x.y1, x.w1, x.h, c.gated ? rgo_gk::EPI_SWIGLU : rgo_gk::EPI_GELU, rgo_gk::OUT_E4M3,
                  c.a_ffn1, c.s_ffn1);
-        g.rng = rq;
+        g.rng = rq_next();
         g.rng_warps = rw;
         if ((e = launch_gemm(g, s)) != cudaSuccess) return e;
         ++n;
         g = gemm(c, M, d, F, x.h, x.w2, x.x, rgo_gk::EPI_NONE, rgo_gk::OUT_E4M3, c.a_ffn2, c.s_ffn2);
-        g.rng = rq;
+        g.rng = rq_next();
         g.rng_warps = rw;
         if ((e = launch_gemm(g, s)) != cudaSuccess) return e;
         ++n;
     }
     g = gemm(c, M, 3 * d, d, x.x, x.wqkv, x.qkv, rgo_gk::EPI_NONE, rgo_gk::OUT_BF16, c.a_qkv, 1.0f);
-    g.rng = rq;
+    g.rng = rq_next();
     g.rng_warps = rw;
     if ((e = launch_gemm(g, s)) != cudaSuccess) return e;
     ++n;

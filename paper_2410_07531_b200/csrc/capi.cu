@@ -70,6 +70,13 @@ int validate_mask(const rgo_mask_desc* d, const char* fn) {
 }  // namespace
 
 namespace rgo {
+HostWorkspace& host_workspace() {
+    static HostWorkspace ws[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return ws[dev & 63];
+}
+
 int num_sms() {
     static int cached[64] = {0};
     int dev = 0;
@@ -198,18 +205,21 @@ int rgo_generate_mask_host_ex(const rgo_mask_desc* d, uint8_t* h_bits, uint64_t 
         const uint64_t e0 = v0 * 128, e1 = std::min(n, v1 * 128);
         const uint64_t b0 = v0 * 16, b1 = std::min(nbytes, v1 * 16);
         cudaSetDevice((prev + static_cast<int>(r % devices)) % ndev);
-        uint8_t* dbuf = nullptr;
-        cudaError_t ce = cudaMalloc(&dbuf, (b1 - b0 + 15) & ~uint64_t{15});
+        // the device's staging workspace (shards sharing a device take turns on it)
+        rgo::HostWorkspace& ws = rgo::host_workspace();
+        std::lock_guard<std::mutex> lk(ws.mu);
+        void* buf = nullptr;
+        cudaError_t ce = ws.get((b1 - b0 + 15) & ~uint64_t{15}, &buf);
         if (ce != cudaSuccess) {
             status[r] = RGO_ENOMEM;
             msgs[r] = cudaGetErrorString(ce);
             return;
         }
+        uint8_t* dbuf = static_cast<uint8_t*>(buf);
         rgo::MaskJob j{dbuf, e1 - e0, d->seed, d->base_offset + e0 / 4, d->threshold,
                        static_cast<int>(d->rounds)};
         ce = rgo::launch_mask(j, rgo::LaunchShape{}, nullptr);
         if (ce == cudaSuccess) ce = cudaMemcpy(h_bits + b0, dbuf, b1 - b0, cudaMemcpyDeviceToHost);
-        cudaFree(dbuf);
         if (ce != cudaSuccess) {
             status[r] = RGO_ECUDA;
             msgs[r] = cudaGetErrorString(ce);

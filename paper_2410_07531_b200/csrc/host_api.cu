@@ -1,7 +1,9 @@
 // host_api.cu -- host-buffer entry points of the C ABI (include/rgo/capi.h):
 // the value-semantics forms the reference's C++ API needs (philox_block,
-// random_attention_input, attention_*, RNGM mask files).  Device staging is
-// allocated and freed inside each call; all arithmetic runs on the GPU.
+// random_attention_input, attention_*, RNGM mask files).  Device staging comes
+// from a per-device grow-only workspace (rgo::host_workspace) or, for the rare
+// philox/random-input helpers, is allocated inside the call; all arithmetic
+// runs on the GPU.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -10,6 +12,7 @@
 #include <cstdio>
 #include <cstring>
 #include <memory>
+#include <mutex>
 
 #include "attn.h"
 #include "rgo/capi.h"
@@ -137,22 +140,31 @@ int rgo_attention_host(const rgo_attn_host_desc* a, const float* h_q, const floa
     if (rgo_device_count() == 0) return set_error(RGO_ENODEV, "no CUDA device: the rgo B200 path has no CPU fallback");
     const int hd = static_cast<int>(a->head_dim), hp = hd <= 64 ? 64 : 128;
     const uint64_t rows = static_cast<uint64_t>(a->slices) * a->seq;
-    DevBuf f, q, k, v, o, bits;
-    RGO_TRY(f.alloc(rows * hd * 4), "attention");
-    for (DevBuf* b : {&q, &k, &v, &o}) RGO_TRY(b->alloc(rows * hp * 2), "attention");
+    if (a->mask_source == RGO_MASK_BITS && !h_bits)
+        return set_error(RGO_EINVAL, "attention_dropout_decoupled: null mask");
+    // one staging allocation per device, reused across calls: f32 rows, q, k, v, o (bf16), bits
+    auto up = [](uint64_t n) { return (n + 255) & ~uint64_t{255}; };
+    const uint64_t f_bytes = up(rows * hd * 4), t_bytes = up(rows * hp * 2),
+                   b_bytes = a->mask_source == RGO_MASK_BITS ? up(bits_bytes) : 0;
+    rgo::HostWorkspace& ws = rgo::host_workspace();
+    std::lock_guard<std::mutex> lk(ws.mu);
+    void* base = nullptr;
+    RGO_TRY(ws.get(f_bytes + 4 * t_bytes + b_bytes, &base), "attention");
+    uint8_t* w8 = static_cast<uint8_t*>(base);
+    float* f = reinterpret_cast<float*>(w8);
+    __nv_bfloat16* ds[4];
+    for (int t = 0; t < 4; ++t) ds[t] = reinterpret_cast<__nv_bfloat16*>(w8 + f_bytes + t * t_bytes);
     const float* hs[3] = {h_q, h_k, h_v};
-    DevBuf* ds[3] = {&q, &k, &v};
     for (int t = 0; t < 3; ++t) {
-        RGO_TRY(cudaMemcpy(f.p, hs[t], rows * hd * 4, cudaMemcpyHostToDevice), "attention");
-        pad_to_bf16<<<blocks_for(rows * hp), 256>>>(f.as<float>(), ds[t]->as<__nv_bfloat16>(), rows, hd, hp);
+        RGO_TRY(cudaMemcpy(f, hs[t], rows * hd * 4, cudaMemcpyHostToDevice), "attention");
+        pad_to_bf16<<<blocks_for(rows * hp), 256>>>(f, ds[t], rows, hd, hp);
         RGO_TRY(cudaGetLastError(), "attention");
     }
     const uint8_t* dbits = nullptr;
     if (a->mask_source == RGO_MASK_BITS) {
-        if (!h_bits) return set_error(RGO_EINVAL, "attention_dropout_decoupled: null mask");
-        RGO_TRY(bits.alloc((bits_bytes + 15) & ~uint64_t{15}), "attention");
-        RGO_TRY(cudaMemcpy(bits.p, h_bits, bits_bytes, cudaMemcpyHostToDevice), "attention");
-        dbits = bits.as<uint8_t>();
+        uint8_t* bits = w8 + f_bytes + 4 * t_bytes;
+        RGO_TRY(cudaMemcpy(bits, h_bits, bits_bytes, cudaMemcpyHostToDevice), "attention");
+        dbits = bits;
     }
     rgo_attn_desc d{};
     d.batch = 1;
@@ -166,12 +178,12 @@ int rgo_attention_host(const rgo_attn_host_desc* a, const float* h_q, const floa
     d.base_offset = a->base_offset;
     d.rounds = a->rounds;
     const long long ss = hp, sh = static_cast<long long>(a->seq) * hp, sb = sh * a->slices;
-    rgo_tensor4 tq{q.p, sb, sh, ss}, tk{k.p, sb, sh, ss}, tv{v.p, sb, sh, ss}, to{o.p, sb, sh, ss};
+    rgo_tensor4 tq{ds[0], sb, sh, ss}, tk{ds[1], sb, sh, ss}, tv{ds[2], sb, sh, ss}, to{ds[3], sb, sh, ss};
     int rc = rgo_attn_fwd(&d, &tq, &tk, &tv, dbits, bits_bytes, &to, nullptr, nullptr);
     if (rc != RGO_OK) return rc;
-    unpad_to_f32<<<blocks_for(rows * hd), 256>>>(o.as<__nv_bfloat16>(), f.as<float>(), rows, hd, hp);
+    unpad_to_f32<<<blocks_for(rows * hd), 256>>>(ds[3], f, rows, hd, hp);
     RGO_TRY(cudaGetLastError(), "attention");
-    RGO_TRY(cudaMemcpy(h_o, f.p, rows * hd * 4, cudaMemcpyDeviceToHost), "attention");
+    RGO_TRY(cudaMemcpy(h_o, f, rows * hd * 4, cudaMemcpyDeviceToHost), "attention");
     return RGO_OK;
 }
 

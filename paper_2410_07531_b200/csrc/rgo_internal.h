@@ -71,6 +71,32 @@ inline cudaError_t ensure_dyn_smem(const void* kernel, int bytes) {
     return e;
 }
 
+// Per-device staging workspace of the host-buffer entry points (the drop-in
+// forms of the reference's value-semantics API): one grow-only device
+// allocation per device, reused across calls instead of cudaMalloc/cudaFree per
+// call.  Callers hold `mu` for the whole call (the host entry points are
+// synchronous, so the buffer is idle again when they return).
+struct HostWorkspace {
+    std::mutex mu;
+    void* p = nullptr;
+    size_t cap = 0;
+    // a buffer of >= n bytes (256-byte aligned); call with mu held
+    cudaError_t get(size_t n, void** out) {
+        if (n > cap) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            cap = 0;
+            const size_t want = n + (n >> 2);  // headroom for slightly larger calls
+            cudaError_t e = cudaMalloc(&p, want);
+            if (e != cudaSuccess) return e;
+            cap = want;
+        }
+        *out = p;
+        return cudaSuccess;
+    }
+};
+HostWorkspace& host_workspace();  // the current device's
+
 int num_sms();
 int mask_kernel_occupancy(int rounds, int block, size_t dyn_smem);
 cudaError_t launch_mask(const MaskJob& j, const LaunchShape& shape, cudaStream_t s);
