@@ -723,6 +723,12 @@ def bench_attention_bwd(rgo, rank, world, peaks):
                      "fwd_tflops": round(flops_f / fwd / 1e9, 1), "bwd_tflops": round(2.5 * flops_f / bwd / 1e9, 1)}
     mask_ms = event_ms(lambda: rgo.generate_mask_device(rgo.MaskLayout(B, H, S, 42, base),
                                                         rgo.KeepThreshold(L["keep_prob"]), 10, out=bits), 5, world)
+    det = event_ms(lambda: rgo.attn_bwd(q, k, v, o, do, lse, dq=g[0], dk=g[1], dv=g[2], work=work, mask_source=1,
+                                        keep_prob=L["keep_prob"], bits=bits, deterministic=True), 5, world)
+    out["bits_deterministic_bwd"] = {
+        "bwd_ms": round(det, 4), "bwd_tflops": round(2.5 * flops_f / det / 1e9, 1),
+        "what": "RGO_ATTN_BWD_DETERMINISTIC: split dK/dV + dQ kernels, dQ accumulated in TMEM (no cross-CTA "
+                "reductions, 7 instead of 5 MMAs per 128x128 block)"}
     out["mask_ms"] = round(mask_ms, 4)
     out["bwd_speedup_bits_vs_fused"] = round(out["philox_fused"]["bwd_ms"] / out["bits"]["bwd_ms"], 4)
     out["fwd_bwd_speedup_bits_vs_fused"] = round(

@@ -181,8 +181,15 @@ typedef struct rgo_attn_desc {
     uint64_t seed;        /* PHILOX: mask layout (batch*heads slices) seed */
     uint64_t base_offset; /* PHILOX: counter of element 0 */
     uint32_t rounds;      /* PHILOX: [1,16] */
-    uint32_t reserved;
+    uint32_t flags;       /* rgo_attn_flags (0 = defaults) */
 } rgo_attn_desc;
+
+/* rgo_attn_desc.flags.  RGO_ATTN_BWD_DETERMINISTIC: head_dim-128 backward in
+ * its split form -- a dK/dV kernel and a dQ kernel that accumulates dQ in
+ * TMEM over all keys (no fp32 reductions across CTAs), so dQ is bitwise
+ * reproducible (and equal between mask bits and inline Philox); slower than
+ * the default (which reduces dQ partials with bulk fp32 adds). */
+typedef enum rgo_attn_flags { RGO_ATTN_BWD_DETERMINISTIC = 1 } rgo_attn_flags;
 
 /* O = softmax(Q K^T * scale) with dropout (denominator over all keys, kept
  * weights / keep_prob), written to o (bf16, same view convention).  d_bits

@@ -66,7 +66,7 @@ class attn_desc(C.Structure):
     _fields_ = [
         ("batch", C.c_uint32), ("heads", C.c_uint32), ("seq", C.c_uint32), ("head_dim", C.c_uint32),
         ("scale", C.c_float), ("mask_source", C.c_int32), ("keep_prob", C.c_double),
-        ("seed", C.c_uint64), ("base_offset", C.c_uint64), ("rounds", C.c_uint32), ("reserved", C.c_uint32),
+        ("seed", C.c_uint64), ("base_offset", C.c_uint64), ("rounds", C.c_uint32), ("flags", C.c_uint32),
     ]
 
 

@@ -82,6 +82,7 @@ struct AttnBwdJob {
     uint64_t seed, base_offset, threshold;
     int rounds;
     void* work;              // attn_bwd_workspace_bytes()
+    bool deterministic;      // head_dim 128: split backward, dQ in TMEM (no cross-CTA reductions)
 };
 
 uint64_t attn_bwd_workspace_bytes(int B, int H, int S, int HD);

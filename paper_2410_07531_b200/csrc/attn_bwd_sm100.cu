@@ -259,6 +259,7 @@ __global__ void bwd_prep_kernel(const __nv_bfloat16* __restrict__ O, long long o
     float* rw = rows + (slice * n_qt + qt) * (2 * BQ);
     rw[rr] = nl;
     rw[BQ + rr] = d;
+    if (!dq_acc) return;  // split backward (v3): dQ accumulates in TMEM, no fp32 accumulator
     float4* acc = reinterpret_cast<float4*>(dq_acc + dq_tile_base(slice, n_qt, qt, HD));
     for (int g = 0; g < HD / 4; ++g) acc[g * BQ + rr] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
 }
@@ -289,7 +290,9 @@ __global__ void bwd_dq_kernel(const float* __restrict__ dq_acc, __nv_bfloat16* _
     *reinterpret_cast<uint4*>(dQ + bb * q_sb + hh * q_sh + static_cast<long long>(r) * q_ss + 8 * g) = out;
 }
 
-template <int HD, int MODE, int R>
+// DQ = false: the dK/dV half of the split backward (launch_attn_bwd3): no dQ
+// MMA, no dS staging in shared memory, no drain -- dQ comes from bwd_dq3_kernel.
+template <int HD, int MODE, int R, bool DQ>
 __global__ void __launch_bounds__(THREADS, 1) bwd_main_kernel(const __grid_constant__ CUtensorMap tmQ,
                                                               const __grid_constant__ CUtensorMap tmK,
                                                               const __grid_constant__ CUtensorMap tmV,
@@ -439,7 +442,7 @@ __global__ void __launch_bounds__(THREADS, 1) bwd_main_kernel(const __grid_const
             const int dst = i % DO_STAGES;
             const uint32_t doff = (dst * SM::TILE) >> 4;
             mbar_wait(smem_u32(&do_full[dst]), (i / DO_STAGES) & 1);
-            if (i > 0) mbar_wait(smem_u32(dq_empty), (i - 1) & 1);
+            if (DQ && i > 0) mbar_wait(smem_u32(dq_empty), (i - 1) & 1);
             tc_fence_after();
             if (elect_one()) {
                 issue_t(tdP, v_kdesc, do_kdesc + doff);
@@ -467,11 +470,14 @@ __global__ void __launch_bounds__(THREADS, 1) bwd_main_kernel(const __grid_const
             tc_fence_after();
             if (elect_one()) {
                 issue_acc(tdK, tdP, q_mdesc + soff, i > 0);
+                if constexpr (DQ) {
 #pragma unroll
-                for (int kk = 0; kk < BKV / 16; ++kk)
-                    mma_f16_ss(tdP, ds_mdesc + ((kk * 2048) >> 4), k_mdesc + ((kk * 2048) >> 4), IDESC_DQ, kk > 0);
+                    for (int kk = 0; kk < BKV / 16; ++kk)
+                        mma_f16_ss(tdP, ds_mdesc + ((kk * 2048) >> 4), k_mdesc + ((kk * 2048) >> 4), IDESC_DQ,
+                                   kk > 0);
+                }
                 tc_commit(smem_u32(&q_empty[st]));
-                tc_commit(smem_u32(dq_full));
+                if constexpr (DQ) tc_commit(smem_u32(dq_full));
                 if (i + 1 == n_qt) tc_commit(smem_u32(acc_full));
             }
             __syncwarp();
@@ -561,15 +567,17 @@ __global__ void __launch_bounds__(THREADS, 1) bwd_main_kernel(const __grid_const
                     dpk[e / 2 + 1] = pack_bf16(ds[2], ds[3]);
                 }
                 tmem_st16(tdP + 16 * c, dpk);
-                // smem dS row (key r), queries 64h + 32c.. : 16-byte units 4c..4c+3 of line r
+                if constexpr (DQ) {
+                    // smem dS row (key r), queries 64h + 32c.. : 16-byte units 4c..4c+3 of line r
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const uint32_t unit = (4 * c + u) ^ sw;
-                    *reinterpret_cast<uint4*>(ds_row + unit * 16) =
-                        make_uint4(dpk[4 * u], dpk[4 * u + 1], dpk[4 * u + 2], dpk[4 * u + 3]);
+                    for (int u = 0; u < 4; ++u) {
+                        const uint32_t unit = (4 * c + u) ^ sw;
+                        *reinterpret_cast<uint4*>(ds_row + unit * 16) =
+                            make_uint4(dpk[4 * u], dpk[4 * u + 1], dpk[4 * u + 2], dpk[4 * u + 3]);
+                    }
                 }
             }
-            fence_proxy_async_smem();
+            if constexpr (DQ) fence_proxy_async_smem();
             tmem_st_wait();
             tc_fence_before();
             __syncwarp();
@@ -605,7 +613,7 @@ __global__ void __launch_bounds__(THREADS, 1) bwd_main_kernel(const __grid_const
                 }
             }
         }
-    } else if (warp >= 12) {  // ------------------------------------------------- dQ drain
+    } else if (DQ && warp >= 12) {  // ------------------------------------------- dQ drain
         // TMEM -> smem staging (64 columns, the accumulator's blocked layout)
         // -> one 32 KiB TMA bulk reduce-add per half.  The second half is held
         // in registers while the first is staged, so TMEM is released before
@@ -1145,13 +1153,329 @@ static cudaError_t launch_main2(const CUtensorMap& q, const CUtensorMap& k, cons
     return cudaGetLastError();
 }
 
-template <int HD, int MODE, int R>
+template <int HD, int MODE, int R, bool DQ = true>
 static cudaError_t launch_main(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
                                const CUtensorMap& dO, const Params& p, cudaStream_t s) {
-    auto kern = bwd_main_kernel<HD, MODE, R>;
+    auto kern = bwd_main_kernel<HD, MODE, R, DQ>;
     if (cudaError_t e = rgo::ensure_dyn_smem(reinterpret_cast<const void*>(kern), Smem<HD>::ALLOC); e != cudaSuccess) return e;
     const unsigned grid = static_cast<unsigned>(p.B) * p.H * p.n_kt;
     kern<<<grid, THREADS, Smem<HD>::ALLOC, s>>>(q, k, v, dO, p);
+    return cudaGetLastError();
+}
+
+
+// ============================================================================
+// K7 split form for head_dim 128 ("v3", launch_attn_bwd3): dK/dV by
+// bwd_main_kernel<128, MODE, R, false> (keys on TMEM lanes, 128-query tiles,
+// 4 MMAs per tile, no dQ) and dQ by the kernel below -- one CTA per (slice,
+// 128-query tile), queries on TMEM lanes, looping over the key tiles:
+//   S  = Q K_j^T    (SS, 128 x 128 x 128)        -> TMEM S[j % 2]
+//   dP = dO V_j^T   (SS)                         -> TMEM dP
+//   P  = 2^(S scale log2e - lse log2e), dS = P o (keep ? dP / p : 0 - D)
+//        (the same elementwise terms as bwd_main; dS bf16 over S[j % 2])
+//   dQ += dS K_j    (TS: A = dS from TMEM, B = K_j MN-major)  -> TMEM dQ
+// dQ accumulates in TMEM over all keys and is written once: no fp32
+// accumulator, no cross-CTA reduction (the 64-query kernel moves 8.6 GB of
+// bulk reduce-adds at the Llama2-7B shape), and every MMA is 128 x 128 x 128
+// (the N = 64 MMAs of the 64-query kernel re-read K/V per 64 queries).  The
+// price is recomputing S and dP (7 MMAs per 128 x 128 block instead of 5).
+// TMEM: S0 [0,128) S1 [128,256) dP [256,384) dQ [384,512).
+// Warps: 0 TMA (Q, dO once; K 3-stage, V 2-stage rings), 1 MMA, 2-3 idle,
+// 4-7 / 8-11: the two column halves (keys [0,64) / [64,128) of each tile) of
+// every query row, one thread per row.
+// ============================================================================
+struct Smem3 {
+    static constexpr int CHUNK = 128 * 128;      // 128 rows x 128 B
+    static constexpr int TILE = 2 * CHUNK;       // 128 rows x 128 bf16
+    static constexpr int K_STAGES = 3;
+    static constexpr int V_STAGES = 2;
+    static constexpr int Q_OFF = 0;
+    static constexpr int DO_OFF = TILE;
+    static constexpr int K_OFF = 2 * TILE;
+    static constexpr int V_OFF = K_OFF + K_STAGES * TILE;
+    static constexpr int BAR_OFF = V_OFF + V_STAGES * TILE;
+    static constexpr int BYTES = BAR_OFF + 256;
+    static constexpr int ALLOC = BYTES + 1023;
+};
+constexpr int THREADS3 = 384;
+
+// 64 keep bits of one query row: keys [idx0, idx0 + 64) of the global layout
+// (n_valid keys valid from idx0), as two LSB-first words.
+template <int MODE, int R>
+__device__ __forceinline__ void row_word64(const Params& p, uint64_t idx0, int n_valid, uint32_t (&kw)[2]) {
+    kw[0] = row_word<MODE, R>(p, idx0, n_valid);
+    kw[1] = row_word<MODE, R>(p, idx0 + 32, n_valid - 32);
+}
+
+template <int MODE, int R>
+__global__ void __launch_bounds__(THREADS3, 1) bwd_dq3_kernel(const __grid_constant__ CUtensorMap tmQ,
+                                                               const __grid_constant__ CUtensorMap tmK,
+                                                               const __grid_constant__ CUtensorMap tmV,
+                                                               const __grid_constant__ CUtensorMap tmdO,
+                                                               const Params p, __nv_bfloat16* __restrict__ dQ,
+                                                               long long q_sb, long long q_sh, long long q_ss) {
+    using SM = Smem3;
+    constexpr int HD = 128;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
+    uint8_t* smem = smem_raw + pad;
+    uint8_t* sQ = smem + SM::Q_OFF;
+    uint8_t* sdO = smem + SM::DO_OFF;
+    uint8_t* sK = smem + SM::K_OFF;
+    uint8_t* sV = smem + SM::V_OFF;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::BAR_OFF);
+    uint64_t* q_full = bars;                     // Q + dO
+    uint64_t* k_full = bars + 1;                 // [3]
+    uint64_t* k_empty = k_full + SM::K_STAGES;   // [3]
+    uint64_t* v_full = k_empty + SM::K_STAGES;   // [2]
+    uint64_t* v_empty = v_full + SM::V_STAGES;   // [2]
+    uint64_t* s_full = v_empty + SM::V_STAGES;   // [2]
+    uint64_t* s_free = s_full + 2;               // [2] both halves read S(j)
+    uint64_t* dp_full = s_free + 2;
+    uint64_t* ds_full = dp_full + 1;
+    uint64_t* dq_done = ds_full + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dq_done + 1);
+
+    const uint32_t warp = warp_id(), lane = lane_id();
+    const int qt = blockIdx.x % p.n_qt;
+    const int bh = blockIdx.x / p.n_qt;
+    const int hh = bh % p.H, bb = bh / p.H;
+    const uint64_t slice = static_cast<uint64_t>(bb) * p.H + hh;
+    const int q0 = qt * BQ;
+    const int n_kt = p.n_kt;
+
+    if (warp == 0 && lane == 0) {
+        mbar_init(smem_u32(q_full), 1);
+        for (int s2 = 0; s2 < SM::K_STAGES; ++s2) {
+            mbar_init(smem_u32(&k_full[s2]), 1);
+            mbar_init(smem_u32(&k_empty[s2]), 1);
+        }
+        for (int s2 = 0; s2 < SM::V_STAGES; ++s2) {
+            mbar_init(smem_u32(&v_full[s2]), 1);
+            mbar_init(smem_u32(&v_empty[s2]), 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(smem_u32(&s_full[b]), 1);
+            mbar_init(smem_u32(&s_free[b]), 8);
+        }
+        mbar_init(smem_u32(dp_full), 1);
+        mbar_init(smem_u32(ds_full), 8);
+        mbar_init(smem_u32(dq_done), 1);
+        fence_mbar_init();
+        tma_prefetch_desc(&tmQ);
+        tma_prefetch_desc(&tmK);
+        tma_prefetch_desc(&tmV);
+        tma_prefetch_desc(&tmdO);
+    }
+    if (warp == 1) tmem_alloc<512>(smem_u32(tmem_slot));
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {  // ------------------------------------------------------------ TMA
+        if (elect_one()) {
+            const uint32_t qb = smem_u32(q_full);
+            mbar_arrive_expect_tx(qb, 2 * SM::TILE);
+            for (int c = 0; c < 2; ++c) {
+                tma_load_4d(smem_u32(sQ + c * SM::CHUNK), &tmQ, qb, c * 64, q0, hh, bb);
+                tma_load_4d(smem_u32(sdO + c * SM::CHUNK), &tmdO, qb, c * 64, q0, hh, bb);
+            }
+        }
+        __syncwarp();
+        for (int j = 0; j < n_kt; ++j) {
+            const int ks = j % SM::K_STAGES, vs = j % SM::V_STAGES;
+            mbar_wait(smem_u32(&k_empty[ks]), ((j / SM::K_STAGES) & 1) ^ 1);
+            if (elect_one()) {
+                const uint32_t kb = smem_u32(&k_full[ks]);
+                mbar_arrive_expect_tx(kb, SM::TILE);
+                for (int c = 0; c < 2; ++c)
+                    tma_load_4d(smem_u32(sK + ks * SM::TILE + c * SM::CHUNK), &tmK, kb, c * 64, j * BKV, hh, bb);
+            }
+            __syncwarp();
+            mbar_wait(smem_u32(&v_empty[vs]), ((j / SM::V_STAGES) & 1) ^ 1);
+            if (elect_one()) {
+                const uint32_t vb = smem_u32(&v_full[vs]);
+                mbar_arrive_expect_tx(vb, SM::TILE);
+                for (int c = 0; c < 2; ++c)
+                    tma_load_4d(smem_u32(sV + vs * SM::TILE + c * SM::CHUNK), &tmV, vb, c * 64, j * BKV, hh, bb);
+            }
+            __syncwarp();
+        }
+    } else if (warp == 1) {  // ----------------------------------------------------- MMA
+        constexpr uint32_t IDESC_S = idesc_make(1, 1, BQ, BKV, 0, 0);  // S, dP: K-major A and B
+        constexpr uint32_t IDESC_Q = idesc_make(1, 1, BQ, HD, 0, 1);   // dQ: A TMEM, B MN-major
+        const uint64_t q_desc = desc_kmajor_sw128(smem_u32(sQ));
+        const uint64_t do_desc = desc_kmajor_sw128(smem_u32(sdO));
+        const uint64_t k_desc = desc_kmajor_sw128(smem_u32(sK));
+        const uint64_t v_desc = desc_kmajor_sw128(smem_u32(sV));
+        const uint64_t k_mdesc = desc_sw128(smem_u32(sK), SM::CHUNK, 1024);
+        const uint32_t tdP = tmem + 256, tdQ = tmem + 384;
+        auto issue_t = [&](uint32_t d, uint64_t a, uint64_t b) {  // 128 x 128 x HD, K-major A and B
+#pragma unroll
+            for (int kk = 0; kk < HD / 16; ++kk) {
+                const uint32_t off = ((kk >> 2) * SM::CHUNK + (kk & 3) * 32) >> 4;
+                mma_f16_ss(d, a + off, b + off, IDESC_S, kk > 0);
+            }
+        };
+        auto issue_s = [&](int j) {
+            const int ks = j % SM::K_STAGES;
+            mbar_wait(smem_u32(&k_full[ks]), (j / SM::K_STAGES) & 1);
+            tc_fence_after();
+            if (elect_one()) {
+                issue_t(tmem + (j & 1) * 128, q_desc, k_desc + ((ks * SM::TILE) >> 4));
+                tc_commit(smem_u32(&s_full[j & 1]));
+            }
+            __syncwarp();
+        };
+        auto issue_dp = [&](int j) {
+            const int vs = j % SM::V_STAGES;
+            mbar_wait(smem_u32(&v_full[vs]), (j / SM::V_STAGES) & 1);
+            tc_fence_after();
+            if (elect_one()) {
+                issue_t(tdP, do_desc, v_desc + ((vs * SM::TILE) >> 4));
+                tc_commit(smem_u32(dp_full));
+                tc_commit(smem_u32(&v_empty[vs]));
+            }
+            __syncwarp();
+        };
+        mbar_wait(smem_u32(q_full), 0);
+        issue_s(0);
+        issue_dp(0);
+        if (n_kt > 1) issue_s(1);
+        for (int j = 0; j < n_kt; ++j) {
+            mbar_wait(smem_u32(ds_full), j & 1);
+            tc_fence_after();
+            if (elect_one()) {  // dQ += dS(j) K_j: dS bf16 pairs over S[j % 2], K_j MN-major
+                const int ks = j % SM::K_STAGES;
+#pragma unroll
+                for (int kk = 0; kk < BKV / 16; ++kk)
+                    mma_f16_ts(tdQ, tmem + (j & 1) * 128 + kk * 8,
+                               k_mdesc + ((ks * SM::TILE + kk * 2048) >> 4), IDESC_Q, (j > 0 || kk > 0) ? 1u : 0u);
+                tc_commit(smem_u32(&k_empty[ks]));
+                if (j + 1 == n_kt) tc_commit(smem_u32(dq_done));
+            }
+            __syncwarp();
+            if (j + 1 < n_kt) issue_dp(j + 1);  // overwrites dP after dQ(j) (in issue order)
+            if (j + 2 < n_kt) issue_s(j + 2);   // overwrites S[j % 2] after dQ(j) read dS(j)
+        }
+    } else if (warp >= 4) {  // --------------------------------------------- P / dS, dQ epilogue
+        const int h = (warp - 4) >> 2;               // key half of every tile
+        const uint32_t qw = warp & 3;
+        const int r = static_cast<int>(qw * 32 + lane);  // query row within the tile
+        const int i = q0 + r;
+        const bool row_valid = i < p.S;
+        const uint32_t lane_base = (qw * 32) << 16;
+        const float* rw = p.rows + (slice * p.n_qt + qt) * (2 * BQ);
+        const float nl = rw[r], Dr = rw[BQ + r];    // -lse*log2e (-inf for padding rows), rowsum(dO o O)
+        const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
+        const float2 nl2 = make_float2(nl, nl);
+        const uint64_t row_base = (slice * p.S + static_cast<uint64_t>(row_valid ? i : 0)) * p.S;
+        uint32_t kw_next[2] = {0u, 0u};
+        if (row_valid) row_word64<MODE, R>(p, row_base + 64 * h, p.S - 64 * h, kw_next);
+        for (int j = 0; j < n_kt; ++j) {
+            const int kc0 = j * BKV + 64 * h;  // first key of this half
+            uint32_t kw[2] = {kw_next[0], kw_next[1]};
+            if (row_valid && j + 1 < n_kt) row_word64<MODE, R>(p, row_base + kc0 + BKV, p.S - (kc0 + BKV), kw_next);
+            const uint32_t tS = tmem + lane_base + (j & 1) * 128;
+            mbar_wait(smem_u32(&s_full[j & 1]), (j >> 1) & 1);
+            tc_fence_after();
+            uint32_t pb[32];  // P as bf16 pairs (the same rounding as bwd_main)
+            {
+                uint32_t s0[32], s1[32];
+                tmem_ld32(tS + 64 * h, s0);
+                tmem_ld32(tS + 64 * h + 32, s1);
+                tmem_ld_wait();
+                reg_fence(s0);
+                reg_fence(s1);
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(smem_u32(&s_free[j & 1]));
+                const int valid = p.S - kc0;  // keys >= valid are padding (last tile only)
+#pragma unroll
+                for (int e = 0; e < 32; e += 2) {
+                    const float2 t0 = __ffma2_rn(make_float2(__uint_as_float(s0[e]), __uint_as_float(s0[e + 1])), sc2, nl2);
+                    const float2 t1 = __ffma2_rn(make_float2(__uint_as_float(s1[e]), __uint_as_float(s1[e + 1])), sc2, nl2);
+                    float a0 = ex2_approx(t0.x), a1 = ex2_approx(t0.y), b0 = ex2_approx(t1.x), b1 = ex2_approx(t1.y);
+                    if (valid < 64) {  // warp-uniform
+                        if (e >= valid) a0 = 0.0f;
+                        if (e + 1 >= valid) a1 = 0.0f;
+                        if (32 + e >= valid) b0 = 0.0f;
+                        if (33 + e >= valid) b1 = 0.0f;
+                    }
+                    pb[e / 2] = pack_bf16(a0, a1);
+                    pb[16 + e / 2] = pack_bf16(b0, b1);
+                }
+            }
+            mbar_wait(smem_u32(dp_full), j & 1);
+            tc_fence_after();
+            uint32_t dsk[32];
+            {
+                uint32_t d0[32], d1[32];
+                tmem_ld32(tmem + lane_base + 256 + 64 * h, d0);
+                tmem_ld32(tmem + lane_base + 256 + 64 * h + 32, d1);
+                tmem_ld_wait();
+                reg_fence(d0);
+                reg_fence(d1);
+#pragma unroll
+                for (int e = 0; e < 32; e += 2) {
+                    float ds[4];
+                    const uint32_t dv[4] = {d0[e], d0[e + 1], d1[e], d1[e + 1]};
+                    const uint32_t pw[2] = {pb[e / 2], pb[16 + e / 2]};
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int col = (u < 2 ? 0 : 32) + e + (u & 1);
+                        const float pv = (u & 1) ? bf16_hi(pw[u >> 1]) : bf16_lo(pw[u >> 1]);
+                        const float dp = ((kw[col >> 5] >> (col & 31)) & 1u) ? __uint_as_float(dv[u]) * p.inv_keep : 0.0f;
+                        ds[u] = pv * (dp - Dr);
+                    }
+                    dsk[e / 2] = pack_bf16(ds[0], ds[1]);
+                    dsk[16 + e / 2] = pack_bf16(ds[2], ds[3]);
+                }
+            }
+            // dS over S[j % 2] columns [32h, 32h+32): both halves must have read S(j) first
+            mbar_wait(smem_u32(&s_free[j & 1]), (j >> 1) & 1);
+            tmem_st32(tS + 32 * h, dsk);
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(ds_full));
+        }
+        // ---- epilogue: dQ = scale * acc -> bf16, columns [64h, 64h + 64) of row i
+        mbar_wait(smem_u32(dq_done), 0);
+        tc_fence_after();
+        __nv_bfloat16* dst = dQ + bb * q_sb + hh * q_sh + static_cast<long long>(row_valid ? i : 0) * q_ss;
+#pragma unroll 1
+        for (int c = 0; c < 2; ++c) {
+            const int col = 64 * h + 32 * c;
+            uint32_t o[32];
+            tmem_ld32(tmem + lane_base + 384 + col, o);
+            tmem_ld_wait_regs(o);
+            uint32_t pk[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e)
+                pk[e] = pack_bf16(__uint_as_float(o[2 * e]) * p.scale, __uint_as_float(o[2 * e + 1]) * p.scale);
+            if (row_valid) {
+                uint4* d4 = reinterpret_cast<uint4*>(dst + col);
+#pragma unroll
+                for (int v = 0; v < 4; ++v) d4[v] = make_uint4(pk[4 * v], pk[4 * v + 1], pk[4 * v + 2], pk[4 * v + 3]);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+template <int MODE, int R>
+static cudaError_t launch_dq3(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v, const CUtensorMap& dO,
+                              const Params& p, __nv_bfloat16* dQ, long long sb, long long sh, long long ss,
+                              cudaStream_t s) {
+    auto kern = bwd_dq3_kernel<MODE, R>;
+    if (cudaError_t e = rgo::ensure_dyn_smem(reinterpret_cast<const void*>(kern), Smem3::ALLOC); e != cudaSuccess)
+        return e;
+    const unsigned grid = static_cast<unsigned>(p.B) * p.H * p.n_qt;
+    kern<<<grid, THREADS3, Smem3::ALLOC, s>>>(q, k, v, dO, p, dQ, sb, sh, ss);
     return cudaGetLastError();
 }
 
@@ -1174,10 +1498,17 @@ static bool tmap4(CUtensorMap* m, const AttnTensor& t, int B, int H, int S, int 
     return make_tmap(m, t.ptr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
-// RGO_BWD_V1=1 (read once per process) runs the 128-query-tile kernel for head
-// dim 128 as well (the 64-query-tile kernel is faster there; same results).
-static bool bwd_force_v1() {
-    static const bool v = getenv("RGO_BWD_V1") != nullptr;
+// Head-dim-128 backward implementation (RGO_BWD_IMPL, read once per process):
+//   2 (default) 64-query tiles, dQ^T double-buffered in TMEM, fp32 bulk reduce-adds
+//   3           split: dK/dV kernel (128-query tiles, 4 MMAs) + dQ kernel (dQ in TMEM);
+//               also selected per call by RGO_ATTN_BWD_DETERMINISTIC
+//   1           128-query tiles with dQ into the dP columns (the head-dim-64 kernel)
+static int bwd_impl() {
+    static const int v = [] {
+        const char* e = getenv("RGO_BWD_IMPL");
+        if (e && (e[0] == '1' || e[0] == '2' || e[0] == '3')) return e[0] - '0';
+        return getenv("RGO_BWD_V1") ? 1 : 2;
+    }();
     return v;
 }
 
@@ -1251,9 +1582,48 @@ static cudaError_t launch_attn_bwd2(const AttnBwdJob& j, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// head_dim 128, split form: prep (row terms) -> dK/dV kernel -> dQ kernel.
+static cudaError_t launch_attn_bwd3(const AttnBwdJob& j, cudaStream_t s) {
+    using namespace rgo_attn_bwd;
+    CUtensorMap tq, tk, tv, tdo;
+    if (!tmap4(&tq, j.q, j.B, j.H, j.S, j.HD) || !tmap4(&tk, j.k, j.B, j.H, j.S, j.HD) ||
+        !tmap4(&tv, j.v, j.B, j.H, j.S, j.HD) || !tmap4(&tdo, j.dout, j.B, j.H, j.S, j.HD))
+        return cudaErrorInvalidResourceHandle;
+    const int n_qt = (j.S + BQ - 1) / BQ;
+    const uint64_t rows = static_cast<uint64_t>(j.B) * j.H * n_qt * BQ;
+    float* rowbuf = static_cast<float*>(j.work);  // [rows][2] fits the workspace's first rows*HD*4 bytes
+    {
+        const unsigned threads = 256;
+        const unsigned grid = static_cast<unsigned>((rows + threads - 1) / threads);
+        bwd_prep_kernel<<<grid, threads, 0, s>>>(static_cast<const __nv_bfloat16*>(j.o.ptr), j.o.sb, j.o.sh, j.o.ss,
+                                                 static_cast<const __nv_bfloat16*>(j.dout.ptr), j.dout.sb, j.dout.sh,
+                                                 j.dout.ss, j.lse, rowbuf, nullptr, j.B, j.H, j.S, n_qt, j.HD);
+        if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return e;
+    }
+    Params p{};
+    fill_params(p, j, n_qt, rowbuf, nullptr);
+    int mode = j.mode;
+    if (mode == rgo_attn::MASK_PHILOX && j.threshold >= (uint64_t{1} << 32)) mode = rgo_attn::MASK_NONE;
+    auto* dq = static_cast<__nv_bfloat16*>(j.dq.ptr);
+    cudaError_t e;
+#define RGO_B3(MODEV, RV)                                                                            \
+    {                                                                                                \
+        e = launch_main<128, MODEV, RV, false>(tq, tk, tv, tdo, p, s);                               \
+        if (e == cudaSuccess) e = launch_dq3<MODEV, RV>(tq, tk, tv, tdo, p, dq, j.dq.sb, j.dq.sh, j.dq.ss, s); \
+    }
+    if (mode == rgo_attn::MASK_NONE) RGO_B3(rgo_attn::MASK_NONE, 0)
+    else if (mode == rgo_attn::MASK_BITS) RGO_B3(rgo_attn::MASK_BITS, 0)
+    else if (j.rounds == 10) RGO_B3(rgo_attn::MASK_PHILOX, 10)
+    else if (j.rounds == 7) RGO_B3(rgo_attn::MASK_PHILOX, 7)
+    else RGO_B3(rgo_attn::MASK_PHILOX, 0)
+#undef RGO_B3
+    return e;
+}
+
 cudaError_t launch_attn_bwd(const AttnBwdJob& j, cudaStream_t s) {
     using namespace rgo_attn_bwd;
-    if (j.HD == 128 && !bwd_force_v1()) return launch_attn_bwd2(j, s);
+    if (j.HD == 128 && (j.deterministic || bwd_impl() == 3)) return launch_attn_bwd3(j, s);
+    if (j.HD == 128 && bwd_impl() == 2) return launch_attn_bwd2(j, s);
     CUtensorMap tq, tk, tv, tdo;
     if (!tmap4(&tq, j.q, j.B, j.H, j.S, j.HD) || !tmap4(&tk, j.k, j.B, j.H, j.S, j.HD) ||
         !tmap4(&tv, j.v, j.B, j.H, j.S, j.HD) || !tmap4(&tdo, j.dout, j.B, j.H, j.S, j.HD))

@@ -457,6 +457,7 @@ int rgo_attn_bwd(const rgo_attn_desc* a, const rgo_tensor4* q, const rgo_tensor4
     j.dv = view_out(dv);
     j.lse = d_lse;
     j.work = d_work;
+    j.deterministic = (a->flags & RGO_ATTN_BWD_DETERMINISTIC) != 0;
     cudaError_t ce = rgo::launch_attn_bwd(j, static_cast<cudaStream_t>(stream));
     return ce == cudaSuccess ? RGO_OK : cuda_fail(ce, "rgo_attn_bwd");
 }

@@ -89,10 +89,12 @@ def attn_fwd(q, k, v, o=None, *, mask_source=MASK_NONE, keep_prob=1.0, bits=None
 
 
 def attn_bwd(q, k, v, o, do, lse, *, mask_source=MASK_NONE, keep_prob=1.0, bits=None, seed=0, base_offset=0,
-             rounds=10, scale=0.0, dq=None, dk=None, dv=None, work=None, stream=None):
+             rounds=10, scale=0.0, dq=None, dk=None, dv=None, work=None, stream=None, deterministic=False):
     """Device-level K7 (csrc/attn_bwd_sm100.cu): dQ, dK, dV (bf16 [B, H, S, D])
     of the K5/K6 forward with the same mask arguments; o and lse are that
-    forward's output and natural-log LSE, do the incoming gradient."""
+    forward's output and natural-log LSE, do the incoming gradient.
+    deterministic=True (head_dim 128): the split backward, dQ accumulated in
+    TMEM with no cross-CTA reductions (bitwise reproducible, slower)."""
     import torch
     B, H, S, D = q.shape
     dev = q.device
@@ -103,7 +105,7 @@ def attn_bwd(q, k, v, o, do, lse, *, mask_source=MASK_NONE, keep_prob=1.0, bits=
     def t4(t):
         return _lib.tensor4(t.data_ptr(), t.stride(0), t.stride(1), t.stride(2))
 
-    a = _lib.attn_desc(B, H, S, D, scale, mask_source, keep_prob, seed, base_offset, rounds, 0)
+    a = _lib.attn_desc(B, H, S, D, scale, mask_source, keep_prob, seed, base_offset, rounds, 1 if deterministic else 0)
     need = _lib.C.c_uint64()
     _lib.check(_lib.lib().rgo_attn_bwd_workspace(a, _lib.C.byref(need)))
     if work is None or work.numel() * work.element_size() < need.value:

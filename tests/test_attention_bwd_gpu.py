@@ -30,14 +30,14 @@ def make_inputs(B, H, S, D, seed, qscale=1.0):
     return [t.bfloat16().cuda() for t in (q, k, v, do)]
 
 
-def run(rgo, q, k, v, do, mode, p=0.9, seed=42, base=0, rounds=10, bits=None):
+def run(rgo, q, k, v, do, mode, p=0.9, seed=42, base=0, rounds=10, bits=None, deterministic=False):
     import torch
     B, H, S, D = q.shape
     lse = torch.empty(B * H * S, dtype=torch.float32, device=q.device)
     o = rgo.attn_fwd(q, k, v, mask_source=mode, keep_prob=p, bits=bits, seed=seed, base_offset=base, rounds=rounds,
                      lse=lse)
     dq, dk, dv = rgo.attn_bwd(q, k, v, o, do, lse, mask_source=mode, keep_prob=p, bits=bits, seed=seed,
-                              base_offset=base, rounds=rounds)
+                              base_offset=base, rounds=rounds, deterministic=deterministic)
     torch.cuda.synchronize()
     return o, dq, dk, dv
 
@@ -153,3 +153,55 @@ def test_random_shapes_fwd_bwd_vs_oracle(rgo, cuda):
         nb = B * H * S * S
         keep = oracle.unpack_keep(bits[: (nb + 7) // 8].cpu().numpy(), B * H, S)
         check_vs_oracle(q, k, v, do, ob, dqb, dkb, dvb, keep, p)
+
+
+@pytest.mark.parametrize("S", [640, 200, 4096])
+def test_split_bwd_dq_deterministic(rgo, cuda, S):
+    """RGO_ATTN_BWD_DETERMINISTIC (head dim 128): the split backward (dK/dV kernel
+    + dQ kernel with dQ accumulated in TMEM) has no fp32 reductions across CTAs,
+    so dQ too is bitwise equal between mask bits and inline Philox and between
+    repeated runs; all of it within 5e-3 of the float64 oracle."""
+    import torch
+    B, H, D = 1, 2, 128
+    q, k, v, do = make_inputs(B, H, S, D, 7, qscale=2.0)
+    bits = rgo.generate_mask_device(rgo.MaskLayout(B, H, S, 3, 99), rgo.KeepThreshold(0.8), 10)
+    ob, dqb, dkb, dvb = run(rgo, q, k, v, do, rgo.ref_attention.MASK_BITS, 0.8, 3, 99, 10, bits, deterministic=True)
+    of, dqf, dkf, dvf = run(rgo, q, k, v, do, rgo.ref_attention.MASK_PHILOX, 0.8, 3, 99, 10, deterministic=True)
+    _, dq2, _, _ = run(rgo, q, k, v, do, rgo.ref_attention.MASK_BITS, 0.8, 3, 99, 10, bits, deterministic=True)
+    assert torch.equal(dqb, dqf) and torch.equal(dqb, dq2)
+    assert torch.equal(dkb, dkf) and torch.equal(dvb, dvf)
+    keep = oracle.unpack_keep(bits[: (B * H * S * S + 7) // 8].cpu().numpy(), B * H, S)
+    check_vs_oracle(q, k, v, do, ob, dqb, dkb, dvb, keep, 0.8)
+
+
+def test_bwd_implementations_agree(rgo, cuda):
+    """The three head-dim-128 backward implementations (RGO_BWD_IMPL 1/2/3, read
+    once per process -> subprocesses) agree: dK/dV bitwise between 1 and 3 (same
+    kernel, same MMA order), dQ within fp32-accumulation differences."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + "/tests")
+import paper_2410_07531_b200 as rgo
+from test_attention_bwd_gpu import make_inputs, run
+q, k, v, do = make_inputs(2, 2, 384, 128, 11, qscale=2.0)
+bits = rgo.generate_mask_device(rgo.MaskLayout(2, 2, 384, 8, 0), rgo.KeepThreshold(0.9), 10)
+o, dq, dk, dv = run(rgo, q, k, v, do, rgo.ref_attention.MASK_BITS, 0.9, 8, 0, 10, bits)
+np.save(sys.argv[2], np.stack([t.float().cpu().numpy() for t in (o, dq, dk, dv)]))
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for impl in ("1", "2", "3"):
+        path = f"/tmp/rgo_bwd_impl{impl}_{os.getpid()}.npy"
+        r = subprocess.run([sys.executable, "-c", code, root, path], env=dict(os.environ, RGO_BWD_IMPL=impl),
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out[impl] = np.load(path)
+        os.remove(path)
+    np.testing.assert_array_equal(out["1"][2:], out["3"][2:])  # dK, dV
+    for impl in ("1", "2"):
+        np.testing.assert_array_equal(out[impl][0], out["3"][0])  # O (same forward)
+        assert rel(out[impl][1], out["3"][1]) < 1e-3             # dQ
+        assert rel(out[impl][2:], out["3"][2:]) < 1e-3
