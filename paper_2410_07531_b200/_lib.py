@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librgo_b200.so")
+# RGO_LIB_PATH: A/B measurements of an alternative build (scripts/diag)
+LIB_PATH = os.environ.get("RGO_LIB_PATH") or os.path.join(_HERE, "librgo_b200.so")
 
 RGO_OK, RGO_EINVAL, RGO_ECUDA, RGO_ENOMEM, RGO_EIO, RGO_ENODEV = range(6)
 
