@@ -158,7 +158,10 @@ __device__ __forceinline__ float2 ex2_poly2(float x0, float x1) {
 // the ALU-bound inline-Philox one, and K5 and K6 must share it to stay bitwise equal).  MUFU.EX2 (16/clk/SM) and the tensor core need the same
 // ~1024 cycles per 128x128 tile, so shifting a share to the idle FMA pipes
 // takes the softmax off the critical path.
-constexpr int POLY_EVERY = 8;
+#ifndef RGO_POLY_EVERY
+#define RGO_POLY_EVERY 8
+#endif
+constexpr int POLY_EVERY = RGO_POLY_EVERY;
 
 template <int HD, int MODE, int R>
 __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ,
