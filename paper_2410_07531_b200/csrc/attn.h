@@ -26,6 +26,22 @@ struct AttnParams {
     long long o_sb, o_sh, o_ss;  // element strides of batch, head, position
     float* lse;              // natural-log LSE per (slice, row), or null
 };
+
+#ifdef __CUDACC__
+// Dropout on a packed bf16 pair: given ksh[t] = kw << t (kw: 32 keep bits,
+// LSB first), returns the half-word mask (0x0000 / 0xFFFF per half) of keep
+// bits (e, e+1), e even.  kw << t puts bit 8b+7-t at the msb of byte b, so
+// PRMT's sign-replicate selectors pick bit e from one shifted copy and bit
+// e+1 from the next: one PRMT per pair (plus 7 shifts per 32 keys) instead
+// of a bit test + select per element; the caller ANDs it into the pair.
+__device__ __forceinline__ uint32_t keep_pair_mask(const uint32_t (&ksh)[8], int e) {
+    constexpr uint32_t kSel[4] = {0xCC88u, 0xDD99u, 0xEEAAu, 0xFFBBu};
+    const int pos = e & 7;
+    uint32_t m;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(m) : "r"(ksh[7 - pos]), "r"(ksh[6 - pos]), "r"(kSel[e >> 3]));
+    return m;
+}
+#endif
 }  // namespace rgo_attn
 
 namespace rgo {

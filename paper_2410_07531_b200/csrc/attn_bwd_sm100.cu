@@ -694,8 +694,24 @@ __global__ void __launch_bounds__(THREADS, 1) bwd_main_kernel(const __grid_const
 //   dQ^T = K^T dS^T (M 128 = head dims, N 64 queries, K 128 keys; both operands
 //          MN-major from smem), drained TMEM -> smem -> 32 KiB TMA bulk
 //          reduce-add, double-buffered staging.
+//
+// K^T in TMEM (RGO_BWD_KT_TMEM, default on): the dQ^T MMA reads its A operand,
+// K^T, from TMEM (TS mode) instead of re-reading the 32 KB K tile from shared
+// memory for every query tile -- the kernel is bound by shared-memory
+// bandwidth (ncu: tensor-core operand reads 56 % + LSU 33 % of the SM's smem
+// wavefronts), and this removes 256 of the 1408 tensor-core wavefronts per
+// tile.  The 64 columns come from the dQ^T double buffer, which single
+// buffering does not need (the drain copies dQ^T(i) out of TMEM right after
+// it completes, a full tile before dQ^T(i+1) is issued).  The dQ-drain warps
+// build K^T once per CTA (thread = head dim, 128 keys -> 64 bf16x2 columns):
+//   TMEM  S^T [0,64)  dP^T [64,128)  dQ^T [128,192)  K^T [192,256)  dV  dK
 // ============================================================================
 constexpr int BQ2 = 64;
+#ifndef RGO_BWD_KT_TMEM
+#define RGO_BWD_KT_TMEM 1
+#endif
+constexpr bool KT_TMEM = RGO_BWD_KT_TMEM != 0;
+constexpr int DQ_BUFS = KT_TMEM ? 1 : 2;  // dQ^T accumulators in TMEM
 
 struct Smem2 {
     static constexpr int KCHUNK = 128 * 128;  // K/V: 128 rows x 128 B per 64-dim chunk
@@ -822,7 +838,8 @@ __global__ void __launch_bounds__(THREADS, 1) bwd_main2_kernel(const __grid_cons
     uint64_t* dq_full = ds_full + 1;   // [2]
     uint64_t* dq_empty = dq_full + 2;  // [2]
     uint64_t* acc_full = dq_empty + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+    uint64_t* kt_full = acc_full + 1;  // K^T in TMEM (KT_TMEM)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(kt_full + 1);
 
     const uint32_t warp = warp_id(), lane = lane_id();
     const int kt = blockIdx.x % p.n_kt;
@@ -848,6 +865,7 @@ __global__ void __launch_bounds__(THREADS, 1) bwd_main2_kernel(const __grid_cons
         mbar_init(smem_u32(dp_full), 1);
         mbar_init(smem_u32(ds_full), 8);
         mbar_init(smem_u32(acc_full), 1);
+        mbar_init(smem_u32(kt_full), 4);
         fence_mbar_init();
         tma_prefetch_desc(&tmQ);
         tma_prefetch_desc(&tmK);
@@ -899,7 +917,8 @@ __global__ void __launch_bounds__(THREADS, 1) bwd_main2_kernel(const __grid_cons
     } else if (warp == 1) {  // ----------------------------------------------------- MMA
         constexpr uint32_t IDESC_T = idesc_make(1, 1, BKV, BQ2, 0, 0);  // S^T, dP^T
         constexpr uint32_t IDESC_ACC = idesc_make(1, 1, BKV, HD, 0, 1); // dV, dK
-        constexpr uint32_t IDESC_DQ = idesc_make(1, 1, HD, BQ2, 1, 1);  // dQ^T
+        // dQ^T: A = K^T MN-major from smem, or (KT_TMEM) from TMEM
+        constexpr uint32_t IDESC_DQ = idesc_make(1, 1, HD, BQ2, KT_TMEM ? 0 : 1, 1);
         const uint64_t k_kdesc = desc_kmajor_sw128(smem_u32(sK));
         const uint64_t v_kdesc = desc_kmajor_sw128(smem_u32(sV));
         const uint64_t q_kdesc = desc_kmajor_sw128(smem_u32(sQ));
@@ -960,15 +979,20 @@ __global__ void __launch_bounds__(THREADS, 1) bwd_main2_kernel(const __grid_cons
                 __syncwarp();
             }
             mbar_wait(smem_u32(ds_full), i & 1);
-            const int b = i & 1;
-            if (i >= 2) mbar_wait(smem_u32(&dq_empty[b]), ((i >> 1) - 1) & 1);
+            const int b = DQ_BUFS == 2 ? (i & 1) : 0;
+            if (i >= DQ_BUFS) mbar_wait(smem_u32(&dq_empty[b]), ((i / DQ_BUFS) - 1) & 1);
+            if (KT_TMEM && i == 0) mbar_wait(smem_u32(kt_full), 0);
             tc_fence_after();
             if (elect_one()) {
                 issue_acc(tdK, tdP, q_mdesc + soff, i > 0);
 #pragma unroll
-                for (int kk = 0; kk < BKV / 16; ++kk)
-                    mma_f16_ss(tmem + 128 + 64 * b, k_mdesc + ((kk * 2048) >> 4), ds_mdesc + ((kk * 2048) >> 4),
-                               IDESC_DQ, kk > 0);
+                for (int kk = 0; kk < BKV / 16; ++kk) {
+                    if constexpr (KT_TMEM)
+                        mma_f16_ts(tmem + 128, tmem + 192 + kk * 8, ds_mdesc + ((kk * 2048) >> 4), IDESC_DQ, kk > 0);
+                    else
+                        mma_f16_ss(tmem + 128 + 64 * b, k_mdesc + ((kk * 2048) >> 4), ds_mdesc + ((kk * 2048) >> 4),
+                                   IDESC_DQ, kk > 0);
+                }
                 tc_commit(smem_u32(&q_empty[st]));
                 tc_commit(smem_u32(&dq_full[b]));
                 if (i + 1 == n_qt) tc_commit(smem_u32(acc_full));
@@ -1012,6 +1036,9 @@ __global__ void __launch_bounds__(THREADS, 1) bwd_main2_kernel(const __grid_cons
                 uint32_t s[32];
                 tmem_ld32(tS, s);
                 tmem_ld_wait_regs(s);
+                uint32_t ksh[8];  // W^T = P with dropped pairs' halves cleared (keep_pair_mask, attn.h)
+#pragma unroll
+                for (int t = 0; t < 8; ++t) ksh[t] = kw << t;
                 uint32_t wpk[16];
 #pragma unroll
                 for (int e = 0; e < 32; e += 4) {
@@ -1024,8 +1051,9 @@ __global__ void __launch_bounds__(THREADS, 1) bwd_main2_kernel(const __grid_cons
                     const float p2 = ex2_approx(t1.x), p3 = ex2_approx(t1.y);
                     pb[e / 2] = pack_bf16(p0, p1);
                     pb[e / 2 + 1] = pack_bf16(p2, p3);
-                    wpk[e / 2] = pack_bf16(((kw >> e) & 1u) ? p0 : 0.0f, ((kw >> (e + 1)) & 1u) ? p1 : 0.0f);
-                    wpk[e / 2 + 1] = pack_bf16(((kw >> (e + 2)) & 1u) ? p2 : 0.0f, ((kw >> (e + 3)) & 1u) ? p3 : 0.0f);
+                    wpk[e / 2] = MODE == MASK_NONE ? pb[e / 2] : pb[e / 2] & rgo_attn::keep_pair_mask(ksh, e);
+                    wpk[e / 2 + 1] =
+                        MODE == MASK_NONE ? pb[e / 2 + 1] : pb[e / 2 + 1] & rgo_attn::keep_pair_mask(ksh, e + 2);
                 }
                 tmem_st16(tS, wpk);
             }
@@ -1104,12 +1132,37 @@ __global__ void __launch_bounds__(THREADS, 1) bwd_main2_kernel(const __grid_cons
         const uint32_t qw = warp & 3;
         const int hd = static_cast<int>(qw * 32 + lane);
         const bool leader = warp == 12 && lane == 0;
+        if constexpr (KT_TMEM) {  // K^T -> TMEM columns [192, 256): lane hd, column c = keys (2c, 2c+1)
+            mbar_wait(smem_u32(kv_full), 0);
+            // K[key][hd] in the SW128 K-major tile: 64-dim chunk hd/64, row = key (128 B),
+            // 16-byte unit (hd%64)/8 XOR (key & 7), element hd%8
+            const uint8_t* kcol = sK + (hd >> 6) * SM::KCHUNK + (hd & 7) * 2;
+            const uint32_t unit = static_cast<uint32_t>((hd & 63) >> 3);
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                uint32_t kt32[32];
+#pragma unroll
+                for (int c = 0; c < 32; ++c) {
+                    const int k0 = 64 * half + 2 * c;
+                    const uint32_t lo = *reinterpret_cast<const uint16_t*>(kcol + k0 * 128 + ((unit ^ (k0 & 7)) << 4));
+                    const uint32_t hi =
+                        *reinterpret_cast<const uint16_t*>(kcol + (k0 + 1) * 128 + ((unit ^ ((k0 + 1) & 7)) << 4));
+                    kt32[c] = lo | (hi << 16);
+                }
+                tmem_st32(tmem + ((qw * 32) << 16) + 192 + 32 * half, kt32);
+            }
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(kt_full));
+        }
         for (int i = 0; i < n_qt; ++i) {
-            const int b = i & 1;
-            mbar_wait(smem_u32(&dq_full[b]), (i >> 1) & 1);
+            const int b = i & 1;                        // staging buffer
+            const int tb = DQ_BUFS == 2 ? b : 0;        // TMEM accumulator
+            mbar_wait(smem_u32(&dq_full[tb]), (i / DQ_BUFS) & 1);
             tc_fence_after();
             uint32_t v0[32], v1[32];
-            const uint32_t taddr = tmem + ((qw * 32) << 16) + 128 + 64 * b;
+            const uint32_t taddr = tmem + ((qw * 32) << 16) + 128 + 64 * tb;
             tmem_ld32(taddr, v0);
             tmem_ld32(taddr + 32, v1);
             tmem_ld_wait();
@@ -1117,7 +1170,7 @@ __global__ void __launch_bounds__(THREADS, 1) bwd_main2_kernel(const __grid_cons
             reg_fence(v1);
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(smem_u32(&dq_empty[b]));  // TMEM buffer b free
+            if (lane == 0) mbar_arrive(smem_u32(&dq_empty[tb]));  // TMEM accumulator free
             if (leader) bulk_wait_read1();  // staging b's previous reduce (tile i-2) read out
             named_bar_sync(1, 128);
             float4* stg = reinterpret_cast<float4*>(smem + SM::STG_OFF + b * SM::STG_BYTES);

@@ -411,12 +411,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(const __grid_const
 #pragma unroll
                 for (int cc = 0; cc < 2; ++cc) {
                     const int c = 2 * h + cc;
-                    // Dropout on the packed bf16 pair: kw << t puts bit 8b+7-t at the
-                    // msb of byte b, so PRMT's sign-replicate selectors turn keep bits
-                    // (e, e+1) into a 0x0000/0xFFFF half-word mask from two shifted
-                    // copies, and one AND applies it (1 PRMT + 1 LOP3 per pair plus 7
-                    // shifts per 32 keys, instead of a bit test + FSEL per element).
-                    uint32_t ksh[8];
+                    uint32_t ksh[8];  // dropout on packed bf16 pairs (keep_pair_mask, attn.h)
 #pragma unroll
                     for (int t = 0; t < 8; ++t) ksh[t] = kw[c] << t;
 #pragma unroll
@@ -435,15 +430,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(const __grid_const
                         rs2 = __fadd2_rn(rs2, make_float2(p0, p1));
                         __nv_bfloat162 hv = __floats2bfloat162_rn(p0, p1);
                         uint32_t pw = *reinterpret_cast<uint32_t*>(&hv);
-                        if (MODE != MASK_NONE) {
-                            const int bsel = e >> 3, pos = e & 7;
-                            constexpr uint32_t kSel[4] = {0xCC88u, 0xDD99u, 0xEEAAu, 0xFFBBu};
-                            uint32_t km;
-                            asm("prmt.b32 %0, %1, %2, %3;"
-                                : "=r"(km)
-                                : "r"(ksh[7 - pos]), "r"(ksh[6 - pos]), "r"(kSel[bsel]));
-                            pw &= km;
-                        }
+                        if (MODE != MASK_NONE) pw &= keep_pair_mask(ksh, e);
                         pk[cc * 16 + (e >> 1)] = pw;
                     }
                 }
