@@ -712,6 +712,17 @@ constexpr int BQ2 = 64;
 #endif
 constexpr bool KT_TMEM = RGO_BWD_KT_TMEM != 0;
 constexpr int DQ_BUFS = KT_TMEM ? 1 : 2;  // dQ^T accumulators in TMEM
+// Keep-bit tiles (MASK_BITS, TMA) travel in their own ring, released by the
+// softmax warps as soon as they hold their words: each tile is 64 rows x 16
+// bytes, SQ/8 bytes apart, and loaded with the Q tile (on q_full) its latency
+// gated the Q ring and with it the tensor core.  Measured at B4 H32 S4096
+// (profiles/r02_bwd_experiments.md): bits 2.98-3.09 -> 2.92-2.95 ms with 2
+// stages; 3/4/8 stages 2.95-3.05 ms; per-lane 4-byte loads 2-4 tiles ahead
+// instead of TMA 3.35-3.51 ms.
+#ifndef RGO_BWD_MSK_STAGES
+#define RGO_BWD_MSK_STAGES 2
+#endif
+constexpr int MSK_STAGES = RGO_BWD_MSK_STAGES;
 
 struct Smem2 {
     static constexpr int KCHUNK = 128 * 128;  // K/V: 128 rows x 128 B per 64-dim chunk
@@ -727,8 +738,8 @@ struct Smem2 {
     static constexpr int STG_BYTES = 128 * BQ2 * 4;
     static constexpr int ROW_OFF = STG_OFF + 2 * STG_BYTES; // per stage: 64 -lse2, 64 D
     static constexpr int MSK_OFF = ROW_OFF + 2 * 512;        // per stage: 64 query rows x 16 B of keep bits
-    static constexpr int BAR_OFF = MSK_OFF + 2 * 1024;
-    static constexpr int BYTES = BAR_OFF + 256;
+    static constexpr int BAR_OFF = MSK_OFF + MSK_STAGES * 1024;
+    static constexpr int BYTES = BAR_OFF + 512;
     static constexpr int ALLOC = BYTES + 1023;
 };
 
@@ -839,7 +850,9 @@ __global__ void __launch_bounds__(THREADS, 1) bwd_main2_kernel(const __grid_cons
     uint64_t* dq_empty = dq_full + 2;  // [2]
     uint64_t* acc_full = dq_empty + 2;
     uint64_t* kt_full = acc_full + 1;  // K^T in TMEM (KT_TMEM)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(kt_full + 1);
+    uint64_t* m_full = kt_full + 1;    // [MSK_STAGES] keep-bit tiles (MASK_BITS, TMA)
+    uint64_t* m_empty = m_full + MSK_STAGES;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(m_empty + MSK_STAGES);
 
     const uint32_t warp = warp_id(), lane = lane_id();
     const int kt = blockIdx.x % p.n_kt;
@@ -866,6 +879,10 @@ __global__ void __launch_bounds__(THREADS, 1) bwd_main2_kernel(const __grid_cons
         mbar_init(smem_u32(ds_full), 8);
         mbar_init(smem_u32(acc_full), 1);
         mbar_init(smem_u32(kt_full), 4);
+        for (int s = 0; s < MSK_STAGES; ++s) {
+            mbar_init(smem_u32(&m_full[s]), 1);
+            mbar_init(smem_u32(&m_empty[s]), 8);
+        }
         fence_mbar_init();
         tma_prefetch_desc(&tmQ);
         tma_prefetch_desc(&tmK);
@@ -889,6 +906,21 @@ __global__ void __launch_bounds__(THREADS, 1) bwd_main2_kernel(const __grid_cons
         }
         __syncwarp();
         const float* rows = p.rows + slice * n_qt * (2 * BQ2);
+        const bool mtma = MODE == MASK_BITS && p.mask_tma;
+        // keep bits of (64 query rows of tile t) x (this CTA's 128 keys) into ring slot t % MSK_STAGES
+        auto load_mask = [&](int t) {
+            const int ms = t % MSK_STAGES;
+            mbar_wait(smem_u32(&m_empty[ms]), ((t / MSK_STAGES) & 1) ^ 1);
+            if (elect_one()) {
+                const uint32_t mb = smem_u32(&m_full[ms]);
+                mbar_arrive_expect_tx(mb, 1024);
+                tma_load_2d(smem_u32(smem + SM::MSK_OFF + ms * 1024), &tmM, mb, kv0 / 8,
+                            static_cast<int>(slice) * p.S + qtile(t) * BQ2);
+            }
+            __syncwarp();
+        };
+        if (mtma)
+            for (int t = 0; t < MSK_STAGES - 1 && t < n_qt; ++t) load_mask(t);
         for (int i = 0; i < n_qt; ++i) {
             const int st = i & 1;
             const uint32_t ph = (i >> 1) & 1;
@@ -896,15 +928,13 @@ __global__ void __launch_bounds__(THREADS, 1) bwd_main2_kernel(const __grid_cons
             mbar_wait(smem_u32(&q_empty[st]), ph ^ 1);
             if (elect_one()) {
                 const uint32_t qb = smem_u32(&q_full[st]);
-                mbar_arrive_expect_tx(qb, SM::QTILE + 512 + (p.mask_tma ? 1024 : 0));
+                mbar_arrive_expect_tx(qb, SM::QTILE + 512);
                 for (int c = 0; c < 2; ++c)
                     tma_load_4d(smem_u32(sQ + st * SM::QTILE + c * SM::QCHUNK), &tmQ, qb, c * 64, qt * BQ2, hh, bb);
                 bulk_load(smem_u32(smem + SM::ROW_OFF + st * 512), rows + qt * (2 * BQ2), 512, qb);
-                if (MODE == MASK_BITS && p.mask_tma)  // keep bits of (64 query rows) x (this CTA's 128 keys)
-                    tma_load_2d(smem_u32(smem + SM::MSK_OFF + st * 1024), &tmM, qb, kv0 / 8,
-                                static_cast<int>(slice) * p.S + qt * BQ2);
             }
             __syncwarp();
+            if (mtma && i + MSK_STAGES - 1 < n_qt) load_mask(i + MSK_STAGES - 1);
             mbar_wait(smem_u32(&do_empty[st]), ph ^ 1);
             if (elect_one()) {
                 const uint32_t db = smem_u32(&do_full[st]);
@@ -1018,10 +1048,31 @@ __global__ void __launch_bounds__(THREADS, 1) bwd_main2_kernel(const __grid_cons
             const int qrow = qtile(i) * BQ2 + 32 * h + static_cast<int>(lane);
             const float* nlse = sRows + st * 128 + 32 * h;
             const float* Dv = nlse + BQ2;
+#if defined(RGO_BWD_DIAG) && (RGO_BWD_DIAG & 1)  // timing diagnostic: no softmax/dS work
+            if (MODE == MASK_BITS && p.mask_tma) {
+                mbar_wait(smem_u32(&m_full[i % MSK_STAGES]), (i / MSK_STAGES) & 1);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(smem_u32(&m_empty[i % MSK_STAGES]));
+            }
+            mbar_wait(smem_u32(&q_full[st]), ph);
+            mbar_wait(smem_u32(s_full), i & 1);
+            tc_fence_after();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(p_full));
+            mbar_wait(smem_u32(dp_full), i & 1);
+            tc_fence_after();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(ds_full));
+            if (true) continue;
+#endif
             uint32_t w = 0;
             if (MODE == MASK_BITS && p.mask_tma) {  // this lane's query row, this warp's 32 keys, from smem
-                mbar_wait(smem_u32(&q_full[st]), ph);  // row terms and mask tile of tile i landed
-                w = reinterpret_cast<const uint32_t*>(smem + SM::MSK_OFF + st * 1024)[(32 * h + lane) * 4 + qw];
+                const int ms = i % MSK_STAGES;
+                mbar_wait(smem_u32(&m_full[ms]), (i / MSK_STAGES) & 1);
+                w = reinterpret_cast<const uint32_t*>(smem + SM::MSK_OFF + ms * 1024)[(32 * h + lane) * 4 + qw];
+                __syncwarp();
+                if (lane == 0) mbar_arrive(smem_u32(&m_empty[ms]));  // slot free (the word is in a register)
+                mbar_wait(smem_u32(&q_full[st]), ph);  // row terms of tile i landed
             } else {
                 if (qrow < p.S)
                     w = row_word<MODE, R>(p, (slice * p.S + qrow) * static_cast<uint64_t>(p.S) + kcol, kvalid);
@@ -1161,6 +1212,11 @@ __global__ void __launch_bounds__(THREADS, 1) bwd_main2_kernel(const __grid_cons
             const int tb = DQ_BUFS == 2 ? b : 0;        // TMEM accumulator
             mbar_wait(smem_u32(&dq_full[tb]), (i / DQ_BUFS) & 1);
             tc_fence_after();
+#if defined(RGO_BWD_DIAG) && (RGO_BWD_DIAG & 2)  // timing diagnostic: no dQ drain/reduction
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&dq_empty[tb]));
+            if (true) continue;
+#endif
             uint32_t v0[32], v1[32];
             const uint32_t taddr = tmem + ((qw * 32) << 16) + 128 + 64 * tb;
             tmem_ld32(taddr, v0);
