@@ -233,9 +233,11 @@ int rgo_random_attention_input_host(uint32_t slices, uint32_t seq, uint32_t head
                                     float* h_q, float* h_k, float* h_v);
 
 /* attention_forward / _fused / _decoupled on reference-layout float arrays
- * (slice, pos, dim), any head_dim <= 128 (zero-padded to 64/128 on device;
- * the softmax scale stays 1/sqrt(head_dim)).  Inputs are rounded to bf16 for
- * the tensor cores; h_bits is the packed mask for RGO_MASK_BITS. */
+ * (slice, pos, dim), replacing ref_attention.hpp:108-146.  head_dim <= 128:
+ * the tcgen05 kernels K5/K6 (zero-padded to 64/128 on device, the softmax
+ * scale stays 1/sqrt(head_dim)), inputs rounded to bf16 for the tensor cores;
+ * head_dim in (128, 1024]: the fp32 CUDA-core kernel K5g on the fp32 arrays.
+ * h_bits is the packed mask for RGO_MASK_BITS. */
 typedef struct rgo_attn_host_desc {
     uint32_t slices, seq, head_dim;
     int32_t mask_source;  /* rgo_mask_source */

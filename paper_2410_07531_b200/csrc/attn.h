@@ -83,6 +83,16 @@ struct AttnJob {
 
 cudaError_t launch_attn_fwd(const AttnJob& j, cudaStream_t s);
 
+// K5g (attn_generic.cu): fp32 CUDA-core forward for head_dim in (128, 1024]
+// -- the drop-in's head dims the tcgen05 kernels do not cover.  q/k/v/o are
+// the reference's slice-major fp32 arrays ([slices][S][HD]); same mask sources
+// and semantics as launch_attn_fwd.
+constexpr uint32_t kGenericMaxHeadDim = 1024;
+cudaError_t launch_attn_generic_f32(const float* q, const float* k, const float* v, float* o, uint32_t slices,
+                                    uint32_t S, uint32_t HD, float scale, int mode, float keep_prob,
+                                    const uint8_t* bits, uint64_t seed, uint64_t threshold, uint64_t base_offset,
+                                    int rounds, cudaStream_t s);
+
 // K7 backward (attn_bwd_sm100.cu): dQ, dK, dV from Q, K, V, the forward
 // output O, its natural-log LSE and dO; same mask sources as the forward.
 struct AttnBwdJob {

@@ -132,16 +132,53 @@ int rgo_random_attention_input_host(uint32_t slices, uint32_t seq, uint32_t head
     return RGO_OK;
 }
 
+// head_dim > 128: the fp32 CUDA-core kernel (K5g) on the reference's own fp32 arrays.
+static int attention_host_generic(const rgo_attn_host_desc* a, const float* h_q, const float* h_k, const float* h_v,
+                                  const uint8_t* h_bits, uint64_t bits_bytes, float* h_o) {
+    const uint64_t n = static_cast<uint64_t>(a->slices) * a->seq * a->head_dim;
+    auto up = [](uint64_t x) { return (x + 255) & ~uint64_t{255}; };
+    const uint64_t f_bytes = up(n * 4), b_bytes = a->mask_source == RGO_MASK_BITS ? up(bits_bytes) : 0;
+    rgo::HostWorkspace& ws = rgo::host_workspace();
+    std::lock_guard<std::mutex> lk(ws.mu);
+    void* base = nullptr;
+    RGO_TRY(ws.get(4 * f_bytes + b_bytes, &base), "attention");
+    uint8_t* w8 = static_cast<uint8_t*>(base);
+    float* d[4];
+    for (int t = 0; t < 4; ++t) d[t] = reinterpret_cast<float*>(w8 + t * f_bytes);
+    const float* hs[3] = {h_q, h_k, h_v};
+    for (int t = 0; t < 3; ++t) RGO_TRY(cudaMemcpy(d[t], hs[t], n * 4, cudaMemcpyHostToDevice), "attention");
+    const uint8_t* dbits = nullptr;
+    if (a->mask_source == RGO_MASK_BITS) {
+        uint8_t* bits = w8 + 4 * f_bytes;
+        RGO_TRY(cudaMemcpy(bits, h_bits, bits_bytes, cudaMemcpyHostToDevice), "attention");
+        dbits = bits;
+    }
+    uint64_t thr = 0;
+    float kp = 1.0f;  // the float keep probability the reference scales by (ref_attention.hpp:120,125)
+    if (a->mask_source != RGO_MASK_NONE) {
+        int rc = rgo_keep_threshold(a->keep_prob, &thr, &kp);
+        if (rc != RGO_OK) return rc;
+    }
+    const float scale = 1.0f / std::sqrt(static_cast<float>(a->head_dim));  // ref_attention.hpp:33
+    RGO_TRY(rgo::launch_attn_generic_f32(d[0], d[1], d[2], d[3], a->slices, a->seq, a->head_dim, scale,
+                                         a->mask_source, kp, dbits, a->seed, thr, a->base_offset,
+                                         a->rounds, nullptr),
+            "attention");
+    RGO_TRY(cudaMemcpy(h_o, d[3], n * 4, cudaMemcpyDeviceToHost), "attention");
+    return RGO_OK;
+}
+
 int rgo_attention_host(const rgo_attn_host_desc* a, const float* h_q, const float* h_k, const float* h_v,
                        const uint8_t* h_bits, uint64_t bits_bytes, float* h_o) {
     if (!a || !h_q || !h_k || !h_v || !h_o) return set_error(RGO_EINVAL, "attention: null argument");
     if (a->slices < 1 || a->seq < 1 || a->head_dim < 1) return set_error(RGO_EINVAL, "attention dims must be >= 1");
-    if (a->head_dim > 128) return set_error(RGO_EINVAL, "attention: head_dim > 128 not supported");
+    if (a->head_dim > rgo::kGenericMaxHeadDim) return set_error(RGO_EINVAL, "attention: head_dim > 1024 not supported");
     if (rgo_device_count() == 0) return set_error(RGO_ENODEV, "no CUDA device: the rgo B200 path has no CPU fallback");
     const int hd = static_cast<int>(a->head_dim), hp = hd <= 64 ? 64 : 128;
     const uint64_t rows = static_cast<uint64_t>(a->slices) * a->seq;
     if (a->mask_source == RGO_MASK_BITS && !h_bits)
         return set_error(RGO_EINVAL, "attention_dropout_decoupled: null mask");
+    if (hd > 128) return attention_host_generic(a, h_q, h_k, h_v, h_bits, bits_bytes, h_o);
     // one staging allocation per device, reused across calls: f32 rows, q, k, v, o (bf16), bits
     auto up = [](uint64_t n) { return (n + 255) & ~uint64_t{255}; };
     const uint64_t f_bytes = up(rows * hd * 4), t_bytes = up(rows * hp * 2),

@@ -65,7 +65,22 @@ def _padded_dim(d: int) -> int:
         return 64
     if d <= 128:
         return 128
-    raise ValueError("head_dim > 128 is not supported by the B200 kernel")
+    raise ValueError("head_dim > 128 is not supported by the tcgen05 kernel")
+
+
+def _run_host(inp: AttentionInput, mask_source, keep_prob, bits, seed, base_offset, rounds):
+    """head_dim > 128: the host entry point the C++ drop-in calls (rgo_attention_host),
+    which runs the fp32 CUDA-core kernel K5g (csrc/attn_generic.cu) on the fp32 arrays."""
+    import ctypes as C
+    S, D, N = inp.seq, inp.head_dim, inp.slices
+    q, k, v = (np.ascontiguousarray(x, np.float32) for x in (inp.q, inp.k, inp.v))
+    o = np.empty(N * S * D, np.float32)
+    b = np.ascontiguousarray(bits, np.uint8) if bits is not None else None
+    ad = _lib.attn_host_desc(N, S, D, mask_source, float(keep_prob), seed, base_offset, rounds, 0)
+    _lib.check(_lib.lib().rgo_attention_host(C.byref(ad), q.ctypes.data, k.ctypes.data, v.ctypes.data,
+                                             b.ctypes.data if b is not None else None,
+                                             b.size if b is not None else 0, o.ctypes.data))
+    return AttentionOutput(N, S, D, o)
 
 
 def attn_fwd(q, k, v, o=None, *, mask_source=MASK_NONE, keep_prob=1.0, bits=None, seed=0, base_offset=0,
@@ -159,6 +174,8 @@ def _run(inp: AttentionInput, mask_source, keep_prob=1.0, bits=None, seed=0, bas
     import torch
     inp.validate()
     S, D, N = inp.seq, inp.head_dim, inp.slices
+    if D > 128:
+        return _run_host(inp, mask_source, keep_prob, bits, seed, base_offset, rounds)
     Dp = _padded_dim(D)
     dev = torch.device("cuda")
 

@@ -159,3 +159,27 @@ def test_counter_carry_and_wrap_fwd_bwd(rgo, cuda, base):
     # and the mask itself is the oracle's
     want = oracle.generate_mask(B, H, S, 99, base, 0.9, 10)
     assert np.array_equal(bits[: want.size].cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("hd", [160, 256, 520])
+def test_large_head_dim_generic_kernel(rgo, cuda, hd):
+    """head_dim > 128 (the reference accepts any head_dim): the drop-in's host entry point
+    (rgo_attention_host) runs the fp32 CUDA-core kernel K5g (csrc/attn_generic.cu) on the fp32
+    arrays -- no bf16 rounding, so within 1e-5 of the oracle; fused == decoupled bitwise (with a
+    base_offset); p = 1 is the plain forward bitwise."""
+    N, S = 3, 200
+    inp = rgo.random_attention_input(N, S, hd, 11)
+    fused = rgo.attention_dropout_fused(inp, 42, 0.9, 10, base_offset=5)
+    mask = rgo.generate_mask(rgo.MaskLayout(1, N, S, 42, 5), rgo.KeepThreshold(0.9), 10)
+    assert fused == rgo.attention_dropout_decoupled(inp, mask, 0.9)
+    want = oracle.attention(inp.q, inp.k, inp.v, N, S, hd, 1, 42, 5, 0.9, 10)
+    assert rel(fused.o, want) < 1e-5
+    plain = rgo.attention_forward(inp)
+    assert rel(plain.o, oracle.attention(inp.q, inp.k, inp.v, N, S, hd, 0)) < 1e-5
+    assert rgo.attention_dropout_fused(inp, 42, 1.0, 10) == plain
+
+
+def test_head_dim_limit(rgo, cuda):
+    inp = rgo.random_attention_input(1, 8, 1025, 3)
+    with pytest.raises(ValueError):
+        rgo.attention_forward(inp)
