@@ -344,6 +344,44 @@ int rgo_block_last_timings(rgo_block* blk, float* ms2);
 int rgo_block_last_timings3(rgo_block* blk, float* ms3);
 int rgo_block_destroy(rgo_block* blk);
 
+/* ------------------------------------------------- tensor-parallel block --
+ * Megatron TP over `size` ranks (ParallelismPlan::tp_degree,
+ * capacity.hpp:14-26): heads split across ranks -- QKV and FFN1 column-
+ * parallel, Proj and FFN2 row-parallel, each followed by an all-reduce done
+ * by the library over peer memory (two-shot: every rank reduces M/size rows
+ * of all ranks' bf16 partial sums, fused with the next GEMM's e4m3
+ * quantisation, then gathers the other ranks' rows).  The rgo_block_desc
+ * keeps the GLOBAL heads/ffn; buffers are the rank's: qkv [M, 3*dl],
+ * attn_o/attn_in [M, dl], attn_o8 [M, dl], h [M, ffn/size], weights wqkv
+ * [3*dl, d] (its heads' q, k, v rows), wo [d, dl], w1 [n1/size, d], w2
+ * [d, ffn/size] (dl = heads/size*head_dim); y1 and x stay [M, d]; mask =
+ * the rank's heads [rank*H/size, ...) of every batch item, compact
+ * (B*H/size*S^2/8 bytes), with the global layout's keep bits and counters.
+ * peer_* hold every rank's buffer as mapped in this process (rgo_ipc_open),
+ * [rank] = its own.  Dense FFN, unchunked, eager (no graph). */
+typedef struct rgo_block_tp {
+    uint32_t size, rank;
+    void* peer_part[8];  /* bf16 [M, d] partial-sum buffers */
+    void* peer_y1[8];    /* e4m3 [M, d] (= each rank's buffers.y1) */
+    void* peer_x[8];     /* e4m3 [M, d] (= each rank's buffers.x) */
+} rgo_block_tp;
+
+int rgo_block_create_tp(const rgo_block_desc* d, const rgo_block_buffers* b, const rgo_block_tp* tp,
+                        int32_t mode, rgo_block** out);
+
+/* One TP step: five segments, the caller's barrier(ctx) across all ranks
+ * between them (called after this rank's segment has completed on the GPU). */
+typedef void (*rgo_barrier_fn)(void* ctx);
+int rgo_block_step_tp(rgo_block* blk, rgo_stream_t stream, rgo_barrier_fn barrier, void* ctx, int32_t* launches);
+
+/* CUDA IPC for the peer buffers: the 64-byte handle of the device allocation
+ * holding d_ptr and d_ptr's byte offset in it (caching allocators sub-allocate);
+ * another process maps the allocation (rgo_ipc_open -> its base; peer access
+ * enabled lazily) and adds the offset; rgo_ipc_close takes the base. */
+int rgo_ipc_handle(const void* d_ptr, uint8_t* handle64, uint64_t* offset);
+int rgo_ipc_open(const uint8_t* handle64, void** d_base);
+int rgo_ipc_close(void* d_base);
+
 #ifdef __cplusplus
 }
 #endif

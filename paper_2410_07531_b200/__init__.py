@@ -14,12 +14,12 @@ from .ref_attention import (AttentionInput, AttentionOutput, EquivCase, EquivRes
                             attention_dropout_fused, attention_forward, attn_bwd, attn_fwd, DropoutAttention, default_equiv_grid,
                             random_attention_input, run_equiv_suite)
 from . import sharding
-from .block import Block
+from .block import Block, TPBlock, shard_weights
 from .gemm import (GemmShape, WorkloadConfig, attention_work, gemm, gemm_shapes, gemm_with_rng,
                    mask_queue_drain, rng_elements, workload_preset)
 
 __all__ = [
-    "Block",
+    "Block", "TPBlock", "shard_weights",
     "AttentionInput", "AttentionOutput", "EquivCase", "EquivResult", "attention_dropout_decoupled",
     "attention_dropout_fused", "attention_forward", "attn_bwd", "attn_fwd", "DropoutAttention", "default_equiv_grid", "random_attention_input",
     "run_equiv_suite",

@@ -91,6 +91,14 @@ class block_desc(C.Structure):
     ]
 
 
+class block_tp(C.Structure):
+    _fields_ = [("size", C.c_uint32), ("rank", C.c_uint32), ("peer_part", C.c_void_p * 8),
+                ("peer_y1", C.c_void_p * 8), ("peer_x", C.c_void_p * 8)]
+
+
+BARRIER_FN = C.CFUNCTYPE(None, C.c_void_p)
+
+
 class block_buffers(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in ("x", "wqkv", "wo", "w1", "w2", "qkv", "attn_o", "attn_o8", "y1", "h",
                                           "mask")] + [("mask_bytes", C.c_uint64), ("counter", C.c_void_p),
@@ -149,6 +157,12 @@ SIGNATURES = {
     "rgo_block_last_timings": (C.c_int, [C.c_void_p, C.c_void_p]),
     "rgo_block_last_timings3": (C.c_int, [C.c_void_p, C.c_void_p]),
     "rgo_block_destroy": (C.c_int, [C.c_void_p]),
+    "rgo_block_create_tp": (C.c_int, [C.POINTER(block_desc), C.POINTER(block_buffers), C.c_void_p, C.c_int32,
+                                      C.c_void_p]),
+    "rgo_block_step_tp": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "rgo_ipc_handle": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64)]),
+    "rgo_ipc_open": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
+    "rgo_ipc_close": (C.c_int, [C.c_void_p]),
     "rgo_philox_blocks_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64]),
     "rgo_random_attention_input_host": (
         C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p]),

@@ -158,3 +158,135 @@ def make_weights(cfg: WorkloadConfig, seed: int, device):
         "w1": _uniform(E * n1 * d, 6, seed, device).view(E * n1, d).to(f8),
         "w2": _uniform(E * d * F, 7, seed, device).view(E * d, F).to(f8),
     }
+
+
+def shard_weights(cfg: WorkloadConfig, weights, size: int, rank: int):
+    """Megatron shards of the full block weights for tensor-parallel rank `rank` of `size`:
+    QKV and FFN1 column-parallel (the rank's heads' q/k/v rows, its F/size FFN columns --
+    for SwiGLU whole [128 gate | 128 up] row tiles), Proj and FFN2 row-parallel (the
+    matching input columns)."""
+    import torch
+    d, F = cfg.heads * cfg.head_dim, cfg.ffn()
+    n1 = 2 * F if cfg.gated else F
+    dl, Fl, n1l = d // size, F // size, n1 // size
+    wqkv = weights["wqkv"]
+    return {
+        "wqkv": torch.cat([wqkv[j * d + rank * dl: j * d + (rank + 1) * dl] for j in range(3)]).contiguous(),
+        "wo": weights["wo"][:, rank * dl:(rank + 1) * dl].contiguous(),
+        "w1": weights["w1"][rank * n1l:(rank + 1) * n1l].contiguous(),
+        "w2": weights["w2"][:, rank * Fl:(rank + 1) * Fl].contiguous(),
+    }
+
+
+class TPBlock:
+    """One tensor-parallel rank of the block (rgo_block_create_tp / rgo_block_step_tp):
+    heads split over `group`'s ranks, QKV/FFN1 column-parallel, Proj/FFN2 row-parallel,
+    the two all-reduces done by the library's own two-shot kernels over peer memory
+    (buffers exchanged with CUDA IPC through `group`); the rank's mask is its heads'
+    slices of the global layout (same keep bits and counters as the unsharded block).
+    `group` (torch.distributed) only carries the IPC handles and the step's barriers."""
+
+    def __init__(self, cfg: WorkloadConfig, mode: str = "in_gemm", seed: int = 42, base_offset: int = 0,
+                 group=None, device="cuda", weights=None, rng_launch=(0, 0, 0)):
+        import torch
+        import torch.distributed as dist
+        self.group = group
+        size, rank = dist.get_world_size(group), dist.get_rank(group)
+        self.size, self.rank, self.cfg, self.mode = size, rank, cfg, mode
+        B, S, H, D = cfg.batch, cfg.seq, cfg.heads, cfg.head_dim
+        d, F = H * D, cfg.ffn()
+        if H % size or F % size:
+            raise ValueError("tp_degree must divide nH and the FFN width")
+        Hl, dl, Fl = H // size, d // size, F // size
+        M = B * S
+        self.M, self.d, self.dl, self.Fl = M, d, dl, Fl
+        f8, bf = torch.float8_e4m3fn, torch.bfloat16
+        dev = torch.device(device)
+        if weights is None:
+            weights = make_weights(cfg, seed, dev)
+        self.weights = shard_weights(cfg, weights, size, rank)
+        self.x = torch.zeros(M, d, dtype=f8, device=dev)
+        self.qkv = torch.empty(M, 3 * dl, dtype=bf, device=dev)
+        full_in = _uniform(M * d, 9, seed, dev).view(M, d).mul_(math.sqrt(3.0)).to(bf)  # Block's attn_in
+        self.attn_in = full_in[:, rank * dl:(rank + 1) * dl].contiguous()
+        del full_in
+        self.attn_o = torch.empty(M, dl, dtype=bf, device=dev)
+        self.attn_o8 = torch.empty(M, dl, dtype=f8, device=dev)
+        self.y1 = torch.zeros(M, d, dtype=f8, device=dev)
+        self.h = torch.empty(M, Fl, dtype=f8, device=dev)
+        self.part = torch.zeros(M, d, dtype=bf, device=dev)
+        self.mask = torch.zeros(B * Hl * S * S // 8, dtype=torch.uint8, device=dev)
+        self.counter = torch.zeros(1, dtype=torch.int64, device=dev)
+        torch.cuda.synchronize()
+        # exchange the peer buffers (CUDA IPC handles through the group)
+        L = _lib.lib()
+        mine = []
+        for t in (self.part, self.y1, self.x):
+            h, off = (C.c_uint8 * 64)(), C.c_uint64()
+            _lib.check(L.rgo_ipc_handle(t.data_ptr(), h, C.byref(off)))
+            mine.append((bytes(h), off.value))
+        allh = [None] * size
+        dist.all_gather_object(allh, mine, group=group)
+        self._opened = {}  # IPC handle -> mapped allocation base (one mapping per peer allocation)
+        tp = _lib.block_tp()
+        tp.size, tp.rank = size, rank
+        for r in range(size):
+            for k, (arr, own) in enumerate(((tp.peer_part, self.part), (tp.peer_y1, self.y1), (tp.peer_x, self.x))):
+                if r == rank:
+                    arr[r] = own.data_ptr()
+                    continue
+                handle, off = allh[r][k]
+                if handle not in self._opened:
+                    p = C.c_void_p()
+                    _lib.check(L.rgo_ipc_open((C.c_uint8 * 64).from_buffer_copy(handle), C.byref(p)))
+                    self._opened[handle] = p.value
+                arr[r] = self._opened[handle] + off
+        self.tp = tp
+        desc = _lib.block_desc()
+        desc.batch, desc.seq, desc.heads, desc.head_dim, desc.ffn = B, S, H, D, F
+        desc.gated = 1 if cfg.gated else 0
+        desc.keep_prob = cfg.keep_prob
+        desc.rounds = cfg.philox_rounds
+        desc.use_graph = 0
+        desc.seed, desc.base_offset = seed, base_offset
+        desc.a_qkv, desc.a_proj = math.sqrt(3.0 / d), math.sqrt(3.0 / d)
+        desc.a_ffn1, desc.a_ffn2 = math.sqrt(3.0 / d), math.sqrt(3.0 / F)
+        desc.s_attn, desc.s_proj, desc.s_ffn1, desc.s_ffn2 = 1.0, 1.0, 2.0, 1.0
+        desc.rng_launch = _lib.launch(*rng_launch, 0)
+        self.desc = desc
+        w = self.weights
+        self._bufs = _lib.block_buffers(self.x.data_ptr(), w["wqkv"].data_ptr(), w["wo"].data_ptr(),
+                                        w["w1"].data_ptr(), w["w2"].data_ptr(), self.qkv.data_ptr(),
+                                        self.attn_o.data_ptr(), self.attn_o8.data_ptr(), self.y1.data_ptr(),
+                                        self.h.data_ptr(), self.mask.data_ptr(), self.mask.numel(),
+                                        self.counter.data_ptr(), None, None, None, self.attn_in.data_ptr(), None)
+        handle = C.c_void_p()
+        _lib.check(L.rgo_block_create_tp(desc, self._bufs, C.byref(tp), MODES[mode], C.byref(handle)))
+        self.handle = handle
+        self._barrier = _lib.BARRIER_FN(lambda _ctx: dist.barrier(group=group))
+
+    def step(self, stream=None) -> int:
+        import torch
+        s = (stream or torch.cuda.current_stream()).cuda_stream
+        n = C.c_int32()
+        _lib.check(_lib.lib().rgo_block_step_tp(self.handle, s, self._barrier, None, C.byref(n)))
+        return n.value
+
+    def last_timings3(self):
+        arr = (C.c_float * 3)()
+        _lib.check(_lib.lib().rgo_block_last_timings3(self.handle, arr))
+        return float(arr[0]), float(arr[1]), float(arr[2])
+
+    def close(self):
+        if getattr(self, "handle", None):
+            _lib.lib().rgo_block_destroy(self.handle)
+            self.handle = None
+        for p in getattr(self, "_opened", {}).values():
+            _lib.lib().rgo_ipc_close(p)
+        self._opened = {}
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

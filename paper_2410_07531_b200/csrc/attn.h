@@ -25,6 +25,7 @@ struct AttnParams {
     void* O;                 // bf16 output rows
     long long o_sb, o_sh, o_ss;  // element strides of batch, head, position
     float* lse;              // natural-log LSE per (slice, row), or null
+    int Hg, h0;              // MASK_PHILOX global slice = b*Hg + h0 + h (AttnJob::Hg)
 };
 
 #ifdef __CUDACC__
@@ -79,6 +80,11 @@ struct AttnJob {
     uint64_t seed, base_offset, threshold;
     int rounds;
     bool pdl;                // programmatic dependent launch after the previous kernel in the stream
+    // Tensor-parallel head window: the launch's H heads are heads [h0, h0 + H) of a
+    // layout with Hg heads per batch item (Hg = 0: the launch's own layout).  Philox
+    // counters (MASK_PHILOX) are the global layout's, slice b*Hg + h0 + h; the bits
+    // (MASK_BITS) are the rank's compact mask, slice b*H + h.
+    int Hg = 0, h0 = 0;
 };
 
 cudaError_t launch_attn_fwd(const AttnJob& j, cudaStream_t s);

@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(const __grid_const
         const uint64_t ri = static_cast<uint64_t>(row_valid ? i : 0);
         const uint64_t row_base = MODE == MASK_BITS
                                       ? (slice * p.bits_rows + ri + (p.bits_rows == p.S ? p.q_row0 : 0)) * p.S
-                                      : (slice * p.S + p.q_row0 + ri) * p.S;
+                                      : ((static_cast<uint64_t>(bb) * p.Hg + p.h0 + hh) * p.S + p.q_row0 + ri) * p.S;
         float m = -INFINITY, l = 0.0f;
         // MASK_BITS: the 16 bytes of tile j+MASK_AHEAD are loaded while tile j is
         // processed (a ring of MASK_AHEAD register quads)
@@ -556,6 +556,9 @@ cudaError_t launch_attn_fwd(const AttnJob& j, cudaStream_t s) {
     p.O = j.o.ptr;
     p.o_sb = j.o.sb; p.o_sh = j.o.sh; p.o_ss = j.o.ss;
     p.lse = j.lse;
+    p.Hg = j.Hg > 0 ? j.Hg : j.H;
+    p.h0 = j.Hg > 0 ? j.h0 : 0;
+    if (p.h0 < 0 || p.h0 + j.H > p.Hg) return cudaErrorInvalidValue;
     int mode = j.mode;
     // keep-all (threshold 2^32) or keep_prob 1: every bit is 1 -> plain path, scale 1/p
     if (mode == MASK_PHILOX && j.threshold >= (uint64_t{1} << 32)) mode = MASK_NONE;

@@ -141,6 +141,56 @@ __global__ void moe_combine_kernel(const __nv_bfloat16* __restrict__ ye, uint8_t
     }
 }
 
+// Tensor-parallel all-reduce over peer memory, two-shot (block_step_tp).
+struct TpPeers {
+    const void* p[rgo::BlockBuffers::MAX_TP];
+};
+
+// Reduce-scatter fused with the next GEMM's quantisation: elements [e0, e0+n)
+// of [M, d]: out[e] = e4m3(scale * sum_p part_p[e]), summed in fp32 in rank
+// order (every rank reduces its own rows, so the order is fixed).  8 elements
+// (16 bytes of every peer's bf16 partial) per thread.
+__global__ void tp_reduce_quant_kernel(const TpPeers parts, int tp, uint8_t* __restrict__ out, uint64_t e0,
+                                       uint64_t n, float scale) {
+    for (uint64_t i = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 8; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x * 8) {
+        float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int r = 0; r < tp; ++r) {
+            const uint4 v = *reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(parts.p[r]) + e0 + i);
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[q]));
+                acc[2 * q] += f.x;
+                acc[2 * q + 1] += f.y;
+            }
+        }
+        uint32_t o[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const __nv_fp8x2_storage_t lo = __nv_cvt_float2_to_fp8x2(
+                make_float2(acc[4 * q] * scale, acc[4 * q + 1] * scale), __NV_SATFINITE, __NV_E4M3);
+            const __nv_fp8x2_storage_t hi = __nv_cvt_float2_to_fp8x2(
+                make_float2(acc[4 * q + 2] * scale, acc[4 * q + 3] * scale), __NV_SATFINITE, __NV_E4M3);
+            o[q] = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
+        }
+        *reinterpret_cast<uint2*>(out + e0 + i) = make_uint2(o[0], o[1]);
+    }
+}
+
+// All-gather of the reduced rows: rank p's block [p*per, (p+1)*per) bytes of
+// every other rank's buffer is copied into dst (16-byte vectors).
+__global__ void tp_gather_kernel(const TpPeers src, int tp, int rank, uint8_t* __restrict__ dst, uint64_t per) {
+    const uint64_t vec = per / 16, n = vec * (tp - 1);
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        int r = static_cast<int>(i / vec);
+        r += r >= rank;
+        const uint64_t off = static_cast<uint64_t>(r) * per + (i % vec) * 16;
+        *reinterpret_cast<uint4*>(dst + off) = *reinterpret_cast<const uint4*>(static_cast<const uint8_t*>(src.p[r]) + off);
+    }
+}
+
 }  // namespace rgo_dev
 
 namespace rgo {
@@ -575,7 +625,7 @@ cudaError_t block_create(const BlockConfig& cfg, const BlockBuffers& buf, int mo
         e = cudaEventCreateWithFlags(&b->ev_chunk[t], cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&b->ev_slot[t], cudaEventDisableTiming);
     }
-    if (e == cudaSuccess && use_graph) {
+    if (e == cudaSuccess && use_graph && cfg.tp_size <= 1) {  // TP steps are host-synchronised segments
         // (kernel attributes and tensor maps are host-side calls, legal during capture;
         // no step is executed here, so creating a block never touches its buffers)
         e = cudaStreamBeginCapture(b->s_main, cudaStreamCaptureModeThreadLocal);
@@ -595,8 +645,171 @@ cudaError_t block_create(const BlockConfig& cfg, const BlockBuffers& buf, int mo
     return cudaSuccess;
 }
 
+// Tensor-parallel step, segment `seg` (0..4) on b.s_main (+ b.s_rng), see block.h.
+static cudaError_t enqueue_tp_segment(Block& b, int seg, int* launches) {
+    const BlockConfig& c = b.cfg;
+    const BlockBuffers& x = b.buf;
+    const int tp = c.tp_size, r = c.tp_rank;
+    const int Hl = c.heads / tp, Fl = c.ffn / tp;
+    const int M = c.batch * c.seq, d = c.heads * c.head_dim, dl = Hl * c.head_dim;
+    const int n1l = c.gated ? 2 * Fl : Fl;
+    const uint64_t sq2 = static_cast<uint64_t>(c.seq) * c.seq;
+    const uint64_t elems = static_cast<uint64_t>(c.batch) * Hl * sq2;  // this rank's compact mask
+    VecWindow hw;  // heads [r*Hl, (r+1)*Hl) of every batch item of the global layout
+    hw.wv = static_cast<uint64_t>(Hl) * sq2 / 128;
+    hw.sv = static_cast<uint64_t>(c.heads) * sq2 / 128;
+    hw.ov = static_cast<uint64_t>(r) * Hl * sq2 / 128;
+    cudaStream_t s = b.s_main;
+    int n = 0;
+    cudaError_t e;
+    RngQueue q{};
+    q.out = x.mask;
+    q.n_vec = elems / 128;
+    q.base_offset = c.base_offset;
+    q.k0 = static_cast<uint32_t>(c.seed);
+    q.k1 = static_cast<uint32_t>(c.seed >> 32);
+    q.thr = static_cast<uint32_t>(c.threshold);
+    q.rounds = c.rounds;
+    q.counter = x.counter;
+    q.win = hw;
+    const RngQueue* rq = b.mode == BLOCK_IN_GEMM ? &q : nullptr;
+    const int rw = c.rng_block ? static_cast<int>(c.rng_block) : auto_rng_warps(c);
+    rgo_dev::TpPeers parts{}, y1s{}, xs{};
+    for (int t = 0; t < tp; ++t) {
+        parts.p[t] = x.peer_part[t];
+        y1s.p[t] = x.peer_y1[t];
+        xs.p[t] = x.peer_x[t];
+    }
+    const uint64_t rows_el = static_cast<uint64_t>(M / tp) * d;  // elements of one rank's row block
+    auto reduce = [&](void* out, float scale) -> cudaError_t {
+        rgo_dev::tp_reduce_quant_kernel<<<stream_grid(rows_el / 8), 256, 0, s>>>(
+            parts, tp, static_cast<uint8_t*>(out), r * rows_el, rows_el, scale);
+        ++n;
+        return cudaGetLastError();
+    };
+    auto gather = [&](const rgo_dev::TpPeers& src, void* dst) -> cudaError_t {
+        rgo_dev::tp_gather_kernel<<<stream_grid(rows_el / 16 * (tp - 1)), 256, 0, s>>>(
+            src, tp, r, static_cast<uint8_t*>(dst), rows_el);
+        ++n;
+        return cudaGetLastError();
+    };
+    GemmJob g;
+    switch (seg) {
+    case 0:  // quant + Proj (row-parallel: K = this rank's dl columns) -> bf16 partial
+        if (b.mode == BLOCK_STREAMS) {
+            if ((e = cudaEventRecord(b.ev_fork, s)) != cudaSuccess) return e;
+            if ((e = cudaStreamWaitEvent(b.s_rng, b.ev_fork, 0)) != cudaSuccess) return e;
+            MaskJob mj{x.mask, elems, c.seed, c.base_offset, c.threshold, c.rounds};
+            mj.vwin = hw;
+            LaunchShape ls;
+            ls.grid = c.rng_grid ? c.rng_grid : static_cast<unsigned>(num_sms());
+            ls.block = c.rng_block ? c.rng_block : 256;
+            ls.dyn_smem = c.rng_smem;
+            if ((e = launch_mask(mj, ls, b.s_rng)) != cudaSuccess) return e;
+            ++n;
+            if ((e = cudaEventRecord(b.ev_rng, b.s_rng)) != cudaSuccess) return e;
+        } else if (b.mode == BLOCK_IN_GEMM) {
+            if ((e = cudaMemsetAsync(x.counter, 0, sizeof(unsigned long long), s)) != cudaSuccess) return e;
+        }
+        if ((e = record_timing(b, 0, s)) != cudaSuccess) return e;
+        if ((e = launch_quant_e4m3(x.attn_in ? x.attn_in : x.attn_o, x.attn_o8, static_cast<uint64_t>(M) * dl,
+                                   c.s_attn, s)) != cudaSuccess)
+            return e;
+        ++n;
+        g = gemm(c, M, d, dl, x.attn_o8, x.wo, x.peer_part[r], rgo_gk::EPI_NONE, rgo_gk::OUT_BF16, c.a_proj, 1.0f);
+        g.rng = rq;
+        g.rng_warps = rw;
+        if ((e = launch_gemm(g, s)) != cudaSuccess) return e;
+        ++n;
+        break;
+    case 1:  // reduce-scatter(Proj) + quantise: this rank's rows of y1
+        if ((e = reduce(x.y1, c.s_proj)) != cudaSuccess) return e;
+        break;
+    case 2:  // all-gather y1, FFN1 (column-parallel) + FFN2 (row-parallel) -> bf16 partial
+        if ((e = gather(y1s, x.y1)) != cudaSuccess) return e;
+        g = gemm(c, M, n1l, d, x.y1, x.w1, x.h, c.gated ? rgo_gk::EPI_SWIGLU : rgo_gk::EPI_GELU, rgo_gk::OUT_E4M3,
+                 c.a_ffn1, c.s_ffn1);
+        g.rng = rq;
+        g.rng_warps = rw;
+        if ((e = launch_gemm(g, s)) != cudaSuccess) return e;
+        ++n;
+        g = gemm(c, M, d, Fl, x.h, x.w2, x.peer_part[r], rgo_gk::EPI_NONE, rgo_gk::OUT_BF16, c.a_ffn2, 1.0f);
+        g.rng = rq;
+        g.rng_warps = rw;
+        if ((e = launch_gemm(g, s)) != cudaSuccess) return e;
+        ++n;
+        break;
+    case 3:  // reduce-scatter(FFN2) + quantise: this rank's rows of x
+        if ((e = reduce(x.x, c.s_ffn2)) != cudaSuccess) return e;
+        break;
+    case 4: {  // all-gather x, QKV (column-parallel: this rank's heads) -> attention of its heads
+        if ((e = gather(xs, x.x)) != cudaSuccess) return e;
+        g = gemm(c, M, 3 * dl, d, x.x, x.wqkv, x.qkv, rgo_gk::EPI_NONE, rgo_gk::OUT_BF16, c.a_qkv, 1.0f);
+        g.rng = rq;
+        g.rng_warps = rw;
+        if ((e = launch_gemm(g, s)) != cudaSuccess) return e;
+        ++n;
+        if ((e = record_timing(b, 1, s)) != cudaSuccess) return e;
+        if (b.mode == BLOCK_IN_GEMM) {
+            if ((e = launch_rng_queue(q, 0, 0, 0, s, false)) != cudaSuccess) return e;
+            ++n;
+        } else if (b.mode == BLOCK_STREAMS) {
+            if ((e = cudaStreamWaitEvent(s, b.ev_rng, 0)) != cudaSuccess) return e;
+        }
+        if ((e = record_timing(b, 3, s)) != cudaSuccess) return e;
+        AttnJob a{};
+        a.B = c.batch; a.H = Hl; a.S = c.seq; a.HD = c.head_dim;
+        a.Hg = c.heads; a.h0 = r * Hl;
+        a.scale = 1.0f / sqrtf(static_cast<float>(c.head_dim));
+        const long long ld = 3LL * dl;
+        const __nv_bfloat16* qkv = static_cast<const __nv_bfloat16*>(x.qkv);
+        a.q = {qkv, static_cast<long long>(c.seq) * ld, c.head_dim, ld};
+        a.k = {qkv + dl, static_cast<long long>(c.seq) * ld, c.head_dim, ld};
+        a.v = {qkv + 2 * dl, static_cast<long long>(c.seq) * ld, c.head_dim, ld};
+        a.o = {x.attn_o, static_cast<long long>(c.seq) * dl, c.head_dim, dl};
+        a.lse = x.lse;
+        a.mode = b.mode == BLOCK_SERIAL_FUSED ? rgo_attn::MASK_PHILOX : rgo_attn::MASK_BITS;
+        a.keep_prob = c.keep_prob;
+        a.bits = x.mask;
+        a.bits_bytes = x.mask_bytes;
+        a.seed = c.seed;
+        a.base_offset = c.base_offset;
+        a.threshold = c.threshold;
+        a.rounds = c.rounds;
+        a.pdl = false;
+        if ((e = launch_attn_fwd(a, s)) != cudaSuccess) return e;
+        ++n;
+        if ((e = record_timing(b, 2, s)) != cudaSuccess) return e;
+        break;
+    }
+    default:
+        return cudaErrorInvalidValue;
+    }
+    *launches += n;
+    return cudaSuccess;
+}
+
+cudaError_t block_step_tp(Block* b, cudaStream_t stream, TpBarrier barrier, void* ctx, int* launches) {
+    if (b->cfg.tp_size < 2 || !barrier) return cudaErrorInvalidValue;
+    cudaError_t e;
+    if ((e = cudaEventRecord(b->ev_in, stream)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(b->s_main, b->ev_in, 0)) != cudaSuccess) return e;
+    int n = 0;
+    for (int seg = 0; seg < 5; ++seg) {
+        if ((e = enqueue_tp_segment(*b, seg, &n)) != cudaSuccess) return e;
+        if (seg < 4) {  // every rank's segment done before any rank reads what it wrote
+            if ((e = cudaStreamSynchronize(b->s_main)) != cudaSuccess) return e;
+            barrier(ctx);
+        }
+    }
+    if ((e = cudaEventRecord(b->ev_out, b->s_main)) != cudaSuccess) return e;
+    if (launches) *launches = n;
+    return cudaStreamWaitEvent(stream, b->ev_out, 0);
+}
+
 // Run one step ordered after `stream` (and before later work on it).
 cudaError_t block_step(Block* b, cudaStream_t stream, int* launches) {
+    if (b->cfg.tp_size > 1) return cudaErrorInvalidValue;  // block_step_tp
     cudaError_t e;
     if ((e = cudaEventRecord(b->ev_in, stream)) != cudaSuccess) return e;
     if ((e = cudaStreamWaitEvent(b->s_main, b->ev_in, 0)) != cudaSuccess) return e;

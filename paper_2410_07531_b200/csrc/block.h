@@ -29,6 +29,14 @@ struct BlockConfig {
     // of window c+1 hidden under stage c's GEMMs, and the live mask is a 2-slot
     // ring of window masks (2/C of the full mask)
     int chunks;
+    // Tensor parallelism (Megatron, capacity.hpp:14-26): tp_size ranks
+    // split the heads (QKV and FFN1 column-parallel, Proj and FFN2 row-parallel).  Rank
+    // tp_rank owns heads [tp_rank*H/tp, ...) of every batch item, their compact mask
+    // (the global layout's keep bits and counters) and an F/tp slice of the FFN; the
+    // Proj and FFN2 partial sums are all-reduced over peer memory (two-shot: each rank
+    // reduces its M/tp rows of every rank's bf16 partial and quantises them to e4m3,
+    // then gathers the other ranks' rows).  heads/ffn/weights/buffers are the rank's.
+    int tp_size = 1, tp_rank = 0;
 };
 
 struct BlockBuffers {
@@ -52,11 +60,25 @@ struct BlockBuffers {
                           // null: attn_o, i.e. each step consumes the previous step's output
     void* qkv_out;  // chunked: bf16 [M, 3d] the step's QKV GEMM output (the step's attention
                     // reads qkv, written by the previous step); counter then has chunks entries
+    // tensor parallel (tp_size > 1): every rank's bf16 [M, d] partial-sum buffer and
+    // its y1 / x (e4m3 [M, d], full d) as mapped in this process ([tp_rank] = own)
+    static constexpr int MAX_TP = 8;
+    void* peer_part[MAX_TP] = {};
+    void* peer_y1[MAX_TP] = {};
+    void* peer_x[MAX_TP] = {};
 };
+
+// Host-side barrier across the tensor-parallel ranks (called between the step's
+// segments, after the rank's stream is synchronised).
+typedef void (*TpBarrier)(void* ctx);
 
 struct Block;
 cudaError_t block_create(const BlockConfig& cfg, const BlockBuffers& buf, int mode, bool use_graph, Block** out);
 cudaError_t block_step(Block* b, cudaStream_t stream, int* launches);
+// Tensor-parallel step (tp_size > 1): five segments separated by barrier(ctx) --
+// quant + Proj | reduce(Proj) | gather + FFN1 + FFN2 | reduce(FFN2) | gather + QKV +
+// attention.  Every rank must call it once per step.
+cudaError_t block_step_tp(Block* b, cudaStream_t stream, TpBarrier barrier, void* ctx, int* launches);
 // Device time of the last step's phases: [0] GEMM window (quant + 4 GEMMs),
 // [1] attention (incl. the RNG join / tail), in ms.
 cudaError_t block_last_timings(Block* b, float* ms2);

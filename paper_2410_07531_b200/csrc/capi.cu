@@ -2,6 +2,7 @@
 // argument validation with the reference's error semantics, error mapping,
 // and kernel launches.  No compute happens on the host; with no CUDA device
 // every compute entry point fails with RGO_ENODEV (there is no CPU fallback).
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -535,6 +536,126 @@ int rgo_block_create(const rgo_block_desc* d, const rgo_block_buffers* b, int32_
     if (ce != cudaSuccess) return cuda_fail(ce, "rgo_block_create");
     *out = new rgo_block{impl};
     return RGO_OK;
+}
+
+int rgo_block_create_tp(const rgo_block_desc* d, const rgo_block_buffers* b, const rgo_block_tp* tp, int32_t mode,
+                        rgo_block** out) {
+    if (!d || !b || !tp || !out) return fail(RGO_EINVAL, "rgo_block_create_tp: null argument");
+    const uint32_t n = tp->size, r = tp->rank;
+    if (n < 2 || n > 8 || r >= n) return fail(RGO_EINVAL, "rgo_block_create_tp: size in [2, 8], rank < size");
+    if (d->heads % n) return fail(RGO_EINVAL, "tp_degree must divide nH");  // capacity.hpp:22-23
+    if (d->experts || d->chunks > 1) return fail(RGO_EINVAL, "rgo_block_create_tp: dense FFN, unchunked step");
+    const uint64_t dl = static_cast<uint64_t>(d->heads / n) * d->head_dim, M = static_cast<uint64_t>(d->batch) * d->seq;
+    if (dl % 128 || (d->ffn / n) % 128 || d->ffn % n || M % (128 * n))
+        return fail(RGO_EINVAL, "rgo_block_create_tp: needs (heads/size)*head_dim %% 128, (ffn/size) %% 128 and "
+                                "batch*seq %% (128*size) == 0");
+    for (uint32_t t = 0; t < n; ++t)
+        if (!tp->peer_part[t] || !tp->peer_y1[t] || !tp->peer_x[t])
+            return fail(RGO_EINVAL, "rgo_block_create_tp: missing peer buffer of rank %u", t);
+    if (tp->peer_y1[r] != b->y1 || tp->peer_x[r] != b->x)
+        return fail(RGO_EINVAL, "rgo_block_create_tp: peer_y1/peer_x[rank] must be this rank's y1/x");
+    {  // the rank's compact mask: B * (H/size) * S^2 bits
+        const uint64_t need = static_cast<uint64_t>(d->batch) * (d->heads / n) * d->seq * static_cast<uint64_t>(d->seq) / 8;
+        if (!b->mask || b->mask_bytes < need || !b->counter || !b->x || !b->wqkv || !b->wo || !b->w1 || !b->w2 ||
+            !b->qkv || !b->attn_o || !b->attn_o8 || !b->y1 || !b->h)
+            return fail(RGO_EINVAL, "rgo_block_create_tp: missing buffer (mask needs %llu bytes)",
+                        static_cast<unsigned long long>(need));
+    }
+    if (mode < RGO_OVERLAP_SERIAL_FUSED || mode > RGO_OVERLAP_NO_RNG)
+        return fail(RGO_EINVAL, "rgo_block_create_tp: bad overlap mode");
+    if (d->head_dim != 64 && d->head_dim != 128) return fail(RGO_EINVAL, "rgo_block_create_tp: head_dim 64/128");
+    if (d->rounds < 1 || d->rounds > 16) return fail(RGO_EINVAL, "rgo_block_create_tp: rounds must be in [1,16]");
+    uint64_t thr = 0;
+    float kp = 0;
+    if (rgo_keep_threshold(d->keep_prob, &thr, &kp) != RGO_OK || thr == 0 || thr >= (uint64_t{1} << 32))
+        return fail(RGO_EINVAL, "rgo_block_create_tp: keep_prob must give 0 < threshold < 2^32");
+    if (mode == RGO_OVERLAP_IN_GEMM) {
+        const uint32_t rw = d->rng_launch.block;
+        if (rw != 0 && rw != 4 && rw != 6 && rw != 8 && rw != 12 && rw != 16)
+            return fail(RGO_EINVAL, "rgo_block_create_tp: IN_GEMM RNG warps per GEMM CTA must be 0/4/6/8/12/16");
+    }
+    if (int e = require_device()) return e;
+    rgo::BlockConfig c{};
+    c.batch = static_cast<int>(d->batch); c.seq = static_cast<int>(d->seq);
+    c.heads = static_cast<int>(d->heads); c.head_dim = static_cast<int>(d->head_dim);
+    c.ffn = static_cast<int>(d->ffn); c.gated = d->gated;
+    c.keep_prob = kp; c.threshold = thr; c.rounds = static_cast<int>(d->rounds);
+    c.seed = d->seed; c.base_offset = d->base_offset;
+    c.a_qkv = d->a_qkv; c.a_proj = d->a_proj; c.a_ffn1 = d->a_ffn1; c.a_ffn2 = d->a_ffn2;
+    c.s_attn = d->s_attn; c.s_proj = d->s_proj; c.s_ffn1 = d->s_ffn1; c.s_ffn2 = d->s_ffn2;
+    c.rng_grid = d->rng_launch.grid; c.rng_block = d->rng_launch.block; c.rng_smem = d->rng_launch.dyn_smem;
+    c.experts = 0; c.top_k = 0; c.chunks = 1;
+    c.tp_size = static_cast<int>(n); c.tp_rank = static_cast<int>(r);
+    rgo::BlockBuffers bb{b->x, b->wqkv, b->wo, b->w1, b->w2, b->qkv, b->attn_o, b->attn_o8, b->y1, b->h,
+                         b->mask, b->mask_bytes, b->counter, b->lse, nullptr, nullptr, b->attn_in, nullptr};
+    for (uint32_t t = 0; t < n; ++t) {
+        bb.peer_part[t] = tp->peer_part[t];
+        bb.peer_y1[t] = tp->peer_y1[t];
+        bb.peer_x[t] = tp->peer_x[t];
+    }
+    rgo::Block* impl = nullptr;
+    cudaError_t ce = rgo::block_create(c, bb, mode, false, &impl);
+    if (ce != cudaSuccess) return cuda_fail(ce, "rgo_block_create_tp");
+    *out = new rgo_block{impl};
+    return RGO_OK;
+}
+
+int rgo_block_step_tp(rgo_block* blk, rgo_stream_t stream, rgo_barrier_fn barrier, void* ctx, int32_t* launches) {
+    if (!blk || !barrier) return fail(RGO_EINVAL, "rgo_block_step_tp: null argument");
+    int n = 0;
+    cudaError_t ce = rgo::block_step_tp(blk->impl, static_cast<cudaStream_t>(stream), barrier, ctx, &n);
+    if (launches) *launches = n;
+    return ce == cudaSuccess ? RGO_OK : cuda_fail(ce, "rgo_block_step_tp");
+}
+
+// Base of the device allocation holding d_ptr (caching allocators sub-allocate: an
+// IPC handle names the whole allocation, so the offset has to travel with it).
+static cudaError_t alloc_base(const void* d_ptr, uintptr_t* base) {
+    using Fn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+    static Fn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        return cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+                       q == cudaDriverEntryPointSuccess
+                   ? reinterpret_cast<Fn>(p)
+                   : nullptr;
+    }();
+    if (!fn) return cudaErrorNotSupported;
+    CUdeviceptr b = 0;
+    size_t sz = 0;
+    if (fn(&b, &sz, reinterpret_cast<CUdeviceptr>(d_ptr)) != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    *base = static_cast<uintptr_t>(b);
+    return cudaSuccess;
+}
+
+int rgo_ipc_handle(const void* d_ptr, uint8_t* handle64, uint64_t* offset) {
+    if (!d_ptr || !handle64 || !offset) return fail(RGO_EINVAL, "rgo_ipc_handle: null argument");
+    if (int e = require_device()) return e;
+    uintptr_t base = 0;
+    cudaError_t ce = alloc_base(d_ptr, &base);
+    if (ce != cudaSuccess) return cuda_fail(ce, "rgo_ipc_handle: allocation base");
+    cudaIpcMemHandle_t h;
+    ce = cudaIpcGetMemHandle(&h, const_cast<void*>(d_ptr));
+    if (ce != cudaSuccess) return cuda_fail(ce, "rgo_ipc_handle");
+    static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    std::memcpy(handle64, &h, 64);
+    *offset = static_cast<uint64_t>(reinterpret_cast<uintptr_t>(d_ptr) - base);
+    return RGO_OK;
+}
+
+int rgo_ipc_open(const uint8_t* handle64, void** d_base) {
+    if (!handle64 || !d_base) return fail(RGO_EINVAL, "rgo_ipc_open: null argument");
+    if (int e = require_device()) return e;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, 64);
+    cudaError_t ce = cudaIpcOpenMemHandle(d_base, h, cudaIpcMemLazyEnablePeerAccess);
+    return ce == cudaSuccess ? RGO_OK : cuda_fail(ce, "rgo_ipc_open");
+}
+
+int rgo_ipc_close(void* d_base) {
+    if (!d_base) return fail(RGO_EINVAL, "rgo_ipc_close: null argument");
+    cudaError_t ce = cudaIpcCloseMemHandle(d_base);
+    return ce == cudaSuccess ? RGO_OK : cuda_fail(ce, "rgo_ipc_close");
 }
 
 int rgo_block_step(rgo_block* blk, rgo_stream_t stream, int32_t* launches) {

@@ -17,6 +17,19 @@ struct LaunchShape {
     size_t dyn_smem = 0;    // extra dynamic smem: throttles CTAs/SM for co-residency
 };
 
+// Vector (128-element unit) index map of a row window: compact chunk vector v ->
+// vector of the full layout.  wv = vectors per slice window, sv = per slice,
+// ov = vector offset of the window's first row.  wv == 0: identity.
+struct VecWindow {
+    uint64_t wv = 0, sv = 0, ov = 0;
+};
+__host__ __device__ inline uint64_t window_vec(const VecWindow& w, uint64_t v) {
+    if (w.wv == 0) return v;
+    const uint64_t s = v < 0xFFFFFFFFull && w.wv <= 0xFFFFFFFFull
+                           ? static_cast<uint64_t>(static_cast<uint32_t>(v) / static_cast<uint32_t>(w.wv))
+                           : v / w.wv;
+    return s * w.sv + w.ov + (v - s * w.wv);
+}
 // One dropout-mask generation job in the reference layout (mask.hpp:24-48).
 struct MaskJob {
     uint8_t* out;           // packed bits, 16-byte aligned
@@ -31,21 +44,13 @@ struct MaskJob {
     // layout with `seq` rows/keys: element (s, i, j) takes the keep bit of the
     // full layout's element (s*seq + row0 + i)*seq + j.  Needs seq % 128 == 0.
     uint32_t win_rows = 0, row0 = 0, seq = 0;
+    // General vector window (wv > 0 overrides the row window): out holds the compact
+    // mask of the layout's vectors window_vec(vwin, v) -- e.g. a tensor-parallel
+    // rank's heads [h0, h0+Hl) of every batch item (wv = Hl*SQ^2/128, sv = nH*SQ^2/128,
+    // ov = h0*SQ^2/128, capacity.hpp:14-26), counters of the full layout.
+    VecWindow vwin{};
 };
 
-// Vector (128-element unit) index map of a row window: compact chunk vector v ->
-// vector of the full layout.  wv = vectors per slice window, sv = per slice,
-// ov = vector offset of the window's first row.  wv == 0: identity.
-struct VecWindow {
-    uint64_t wv = 0, sv = 0, ov = 0;
-};
-__host__ __device__ inline uint64_t window_vec(const VecWindow& w, uint64_t v) {
-    if (w.wv == 0) return v;
-    const uint64_t s = v < 0xFFFFFFFFull && w.wv <= 0xFFFFFFFFull
-                           ? static_cast<uint64_t>(static_cast<uint32_t>(v) / static_cast<uint32_t>(w.wv))
-                           : v / w.wv;
-    return s * w.sv + w.ov + (v - s * w.wv);
-}
 inline VecWindow make_window(uint32_t win_rows, uint32_t row0, uint32_t seq) {
     VecWindow w;
     if (win_rows == 0) return w;

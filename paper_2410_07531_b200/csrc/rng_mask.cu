@@ -185,8 +185,9 @@ cudaError_t launch_mask(const MaskJob& j, const LaunchShape& shape_in, cudaStrea
     }
     const uint32_t thr = static_cast<uint32_t>(j.threshold);
     const uint64_t n_vec = n / 128;
-    const VecWindow win = make_window(j.win_rows, j.row0, j.seq);
+    const VecWindow win = j.vwin.wv ? j.vwin : make_window(j.win_rows, j.row0, j.seq);
     if (j.win_rows && (j.seq % 128 || n % 128)) return cudaErrorInvalidValue;
+    if (j.vwin.wv && n % 128) return cudaErrorInvalidValue;
     if (n_vec > 0) {
         LaunchShape ls = shape_in;
         if (ls.block == 0) ls.block = 256;
