@@ -18,6 +18,7 @@ struct AttnParams {
     const uint8_t* bits;     // MASK_BITS: packed mask, reference layout
     uint64_t bits_bytes;
     int bits_aligned;        // SQ % 128 == 0 and 16-byte aligned bits
+    int mask_tma;            // MASK_BITS: keep-bit tiles arrive by TMA (bits_aligned, the kernel's tmM)
     uint32_t k0, k1;         // MASK_PHILOX: key
     uint64_t base_offset;
     uint32_t thr;            // threshold < 2^32

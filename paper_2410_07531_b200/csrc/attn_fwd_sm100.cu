@@ -29,6 +29,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstring>
 
 #include "attn.h"
 #include "philox.cuh"
@@ -49,6 +50,18 @@ constexpr int SOFTMAX_REGS = 224;   // ... and of each softmax warpgroup (4*56 +
 constexpr uint32_t TMEM_COLS = 512;
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
 
+// MASK_BITS with SQ % 128 == 0: the keep-bit tiles (128 query rows x 16 bytes per
+// Q tile and KV step, the mask viewed as a 2-D byte array) arrive by TMA in a ring
+// of MSK_STAGES, MSK_STAGES - 1 KV steps ahead, instead of per-thread 16-byte
+// loads that touch 32 rows per warp instruction (RGO_FWD_MASK_TMA=0: the loads).
+#ifndef RGO_FWD_MASK_TMA
+#define RGO_FWD_MASK_TMA 1
+#endif
+#ifndef RGO_FWD_MSK_STAGES
+#define RGO_FWD_MSK_STAGES 4
+#endif
+constexpr int MSK_STAGES = RGO_FWD_MSK_STAGES;
+
 template <int HD>
 struct Smem {
     static constexpr int CHUNK = 128 * 128;            // one 64-dH (128 B) column block of 128 rows
@@ -56,7 +69,8 @@ struct Smem {
     static constexpr int Q_OFF = 0;
     static constexpr int K_OFF = 2 * TILE;
     static constexpr int V_OFF = K_OFF + KV_STAGES * TILE;
-    static constexpr int BAR_OFF = V_OFF + KV_STAGES * TILE;
+    static constexpr int MSK_OFF = V_OFF + KV_STAGES * TILE;      // keep-bit tiles: [stage][Q tile][128 rows][16 B]
+    static constexpr int BAR_OFF = MSK_OFF + MSK_STAGES * 2 * 2048;
     static constexpr int BYTES = BAR_OFF + 256 + 1024;
 };
 
@@ -174,6 +188,7 @@ template <int HD, int MODE, int R>
 __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ,
                                                               const __grid_constant__ CUtensorMap tmK,
                                                               const __grid_constant__ CUtensorMap tmV,
+                                                              const __grid_constant__ CUtensorMap tmM,
                                                               const AttnParams p) {
     using SM = Smem<HD>;
     extern __shared__ uint8_t smem_raw[];
@@ -191,7 +206,10 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(const __grid_const
     uint64_t* p_full = s_full + 2;           // [2]
     uint64_t* o_done = p_full + 2;           // [2]
     uint64_t* p_half = o_done + 2;           // [2] first 64 P columns in TMEM
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_half + 2);
+    uint64_t* m_full = p_half + 2;           // [MSK_STAGES] keep-bit tiles (MASK_BITS, TMA)
+    uint64_t* m_empty = m_full + MSK_STAGES;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(m_empty + MSK_STAGES);
+    static_assert((17 + 2 * MSK_STAGES) * 8 + 4 <= 256, "barrier area");
 
     const uint32_t warp = warp_id(), lane = lane_id();
     const int pair = blockIdx.x % p.n_pairs;
@@ -213,6 +231,10 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(const __grid_const
             mbar_init(smem_u32(&p_full[w]), 4);
             mbar_init(smem_u32(&o_done[w]), 1);
             mbar_init(smem_u32(&p_half[w]), 4);
+        }
+        for (int t = 0; t < MSK_STAGES; ++t) {
+            mbar_init(smem_u32(&m_full[t]), 1);
+            mbar_init(smem_u32(&m_empty[t]), 8);
         }
         fence_mbar_init();
         tma_prefetch_desc(&tmQ);
@@ -238,6 +260,23 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(const __grid_const
                         tma_load_4d(smem_u32(sQ + w * SM::TILE + c * SM::CHUNK), &tmQ, qb, c * 64, q0 + w * BQ, hh, bb);
             }
             __syncwarp();
+            const bool mtma = MODE == MASK_BITS && p.mask_tma;
+            // keep bits of (this CTA's 2 x 128 query rows) x (KV tile t) into ring slot t % MSK_STAGES
+            const int mrow = static_cast<int>((static_cast<uint64_t>(bb) * p.H + hh) * p.bits_rows) +
+                             (p.bits_rows == p.S ? p.q_row0 : 0) + q0;
+            auto load_mask = [&](int t) {
+                const int ms = t % MSK_STAGES;
+                mbar_wait(smem_u32(&m_empty[ms]), ((t / MSK_STAGES) & 1) ^ 1);
+                if (elect_one()) {
+                    const uint32_t mb = smem_u32(&m_full[ms]);
+                    mbar_arrive_expect_tx(mb, 2 * 2048);
+                    for (int w = 0; w < 2; ++w)
+                        tma_load_2d(smem_u32(smem + SM::MSK_OFF + (ms * 2 + w) * 2048), &tmM, mb, t * 16, mrow + w * BQ);
+                }
+                __syncwarp();
+            };
+            if (mtma)
+                for (int t = 0; t < MSK_STAGES - 1 && t < n_kv; ++t) load_mask(t);
             int ks = 0, vs = 0;
             uint32_t kph = 0, vph = 0;
             for (int j = 0; j < n_kv; ++j) {
@@ -259,6 +298,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(const __grid_const
                 }
                 __syncwarp();
                 if (++vs == KV_STAGES) { vs = 0; vph ^= 1; }
+                if (mtma && j + MSK_STAGES - 1 < n_kv) load_mask(j + MSK_STAGES - 1);
             }
         } else if (warp == 1) {  // MMA issuer (whole warp loops, one lane issues)
             constexpr uint32_t IDESC_S = idesc_make(1, 1, BQ, BKV, 0, 0);
@@ -354,12 +394,21 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(const __grid_const
 #pragma unroll
         for (int a = 0; a < MASK_AHEAD; ++a) {
             kw_ring[a][0] = kw_ring[a][1] = kw_ring[a][2] = kw_ring[a][3] = 0u;
-            if (MODE == MASK_BITS && row_valid && a < n_kv) keep_bits<MODE, R>(p, row_base + a * BKV, kw_ring[a]);
+            if (MODE == MASK_BITS && !p.mask_tma && row_valid && a < n_kv)
+                keep_bits<MODE, R>(p, row_base + a * BKV, kw_ring[a]);
         }
         for (int j = 0; j < n_kv; ++j) {
             const int j0 = j * BKV;
             uint32_t kw[4];
-            if constexpr (MODE == MASK_BITS) {
+            if (MODE == MASK_BITS && p.mask_tma) {  // this row's 16 bytes of the TMA'd tile
+                const int ms = j % MSK_STAGES;
+                mbar_wait(smem_u32(&m_full[ms]), (j / MSK_STAGES) & 1);
+                const uint4 v = *reinterpret_cast<const uint4*>(smem + SM::MSK_OFF + (ms * 2 + w) * 2048 + row * 16);
+                kw[0] = v.x; kw[1] = v.y; kw[2] = v.z; kw[3] = v.w;
+                __syncwarp();
+                if (lane == 0) mbar_arrive(smem_u32(&m_empty[ms]));  // slot free (the words are in registers)
+                if (!row_valid) kw[0] = kw[1] = kw[2] = kw[3] = 0;
+            } else if constexpr (MODE == MASK_BITS) {
 #pragma unroll
                 for (int t = 0; t < 4; ++t) kw[t] = kw_ring[0][t];
 #pragma unroll
@@ -496,8 +545,8 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(const __grid_const
 }
 
 template <int HD, int MODE, int R>
-static cudaError_t launch_t(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v, const AttnParams& p,
-                            cudaStream_t s, bool pdl) {
+static cudaError_t launch_t(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v, const CUtensorMap& m,
+                            const AttnParams& p, cudaStream_t s, bool pdl) {
     auto kern = attn_fwd_kernel<HD, MODE, R>;
     if (cudaError_t e = rgo::ensure_dyn_smem(reinterpret_cast<const void*>(kern), Smem<HD>::BYTES); e != cudaSuccess)
         return e;
@@ -512,7 +561,7 @@ static cudaError_t launch_t(const CUtensorMap& q, const CUtensorMap& k, const CU
     cfg.stream = s;
     cfg.attrs = at;
     cfg.numAttrs = pdl ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, kern, q, k, v, p);
+    return cudaLaunchKernelEx(&cfg, kern, q, k, v, m, p);
 }
 
 }  // namespace rgo_attn
@@ -562,8 +611,20 @@ cudaError_t launch_attn_fwd(const AttnJob& j, cudaStream_t s) {
     int mode = j.mode;
     // keep-all (threshold 2^32) or keep_prob 1: every bit is 1 -> plain path, scale 1/p
     if (mode == MASK_PHILOX && j.threshold >= (uint64_t{1} << 32)) mode = MASK_NONE;
+    // keep-bit tiles by TMA: the mask as a 2-D byte array [B*H*bits_rows rows][S/8 bytes],
+    // box = 16 bytes (128 keys) x 128 query rows
+    CUtensorMap tm;
+    std::memset(&tm, 0, sizeof(tm));
+    p.mask_tma = 0;
+    if (RGO_FWD_MASK_TMA && mode == MASK_BITS && p.bits_aligned) {
+        const uint64_t dims[2] = {static_cast<uint64_t>(j.S) / 8, static_cast<uint64_t>(j.B) * j.H * p.bits_rows};
+        const uint64_t strides[1] = {static_cast<uint64_t>(j.S) / 8};
+        const uint32_t box[2] = {16, static_cast<uint32_t>(BQ)};
+        p.mask_tma = make_tmap(&tm, j.bits, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, dims, strides, box,
+                               CU_TENSOR_MAP_SWIZZLE_NONE) ? 1 : 0;
+    }
 #define RGO_A(HDV, MODEV, RV) \
-    if (j.HD == HDV && mode == MODEV) return launch_t<HDV, MODEV, RV>(tq, tk, tv, p, s, j.pdl);
+    if (j.HD == HDV && mode == MODEV) return launch_t<HDV, MODEV, RV>(tq, tk, tv, tm, p, s, j.pdl);
     RGO_A(128, MASK_NONE, 0)
     RGO_A(64, MASK_NONE, 0)
     RGO_A(128, MASK_BITS, 0)
