@@ -132,3 +132,48 @@ def test_fnv1a64_via_capi(rgo, golden, mask_blobs):
     for m in [x for x in golden["masks"] if x.get("blob")][:8]:
         assert f"{rgo.mask.fnv1a64(mask_blobs[m['blob']]):016x}" == m["fnv"]
     assert rgo.mask.fnv1a64(np.zeros(0, np.uint8)) == 0xcbf29ce484222325
+
+
+def test_block_create_tp_validation(rgo):
+    """rgo_block_create_tp (tensor-parallel block) rejects bad plans before touching any buffer or
+    device: tp size/rank, tp_degree not dividing nH (capacity.hpp:22-23), per-rank widths that
+    break the GEMM tiling, missing peer buffers, and peer[rank] not being the rank's own y1/x."""
+    lib = rgo._lib.lib()
+    E = rgo._lib.RGO_EINVAL
+    h = C.c_void_p()
+    bufs = rgo._lib.block_buffers()
+    d = _block_desc(rgo)
+    d.heads, d.seq, d.ffn = 4, 512, 512
+    tp = rgo._lib.block_tp()
+    for size, rank in ((1, 0), (9, 0), (2, 2)):
+        tp.size, tp.rank = size, rank
+        assert lib.rgo_block_create_tp(d, bufs, C.byref(tp), 2, C.byref(h)) == E
+        assert b"size" in lib.rgo_last_error()
+    tp.size, tp.rank = 3, 0
+    assert lib.rgo_block_create_tp(d, bufs, C.byref(tp), 2, C.byref(h)) == E
+    assert b"tp_degree must divide nH" in lib.rgo_last_error()
+    tp.size = 4  # one head (128 columns) per rank
+    d.ffn = 256  # ffn/size = 64: not a multiple of 128
+    assert lib.rgo_block_create_tp(d, bufs, C.byref(tp), 2, C.byref(h)) == E
+    assert b"(ffn/size)" in lib.rgo_last_error()
+    d.ffn = 512
+    assert lib.rgo_block_create_tp(d, bufs, C.byref(tp), 2, C.byref(h)) == E
+    assert b"missing peer buffer" in lib.rgo_last_error()
+    for t in range(4):
+        tp.peer_part[t] = tp.peer_y1[t] = tp.peer_x[t] = 0x1000 * (t + 1)
+    assert lib.rgo_block_create_tp(d, bufs, C.byref(tp), 2, C.byref(h)) == E
+    assert b"this rank's y1/x" in lib.rgo_last_error()
+
+
+def test_ipc_and_large_head_dim_validation(rgo):
+    lib = rgo._lib.lib()
+    E = rgo._lib.RGO_EINVAL
+    off = C.c_uint64()
+    assert lib.rgo_ipc_handle(None, None, C.byref(off)) == E
+    assert lib.rgo_ipc_open(None, None) == E
+    assert lib.rgo_ipc_close(None) == E
+    # the drop-in attention accepts any head_dim up to 1024 (K5g above 128); beyond: invalid
+    ad = rgo._lib.attn_host_desc(1, 8, 1025, 0, 1.0, 0, 0, 7, 0)
+    x = (C.c_float * 16)()
+    assert lib.rgo_attention_host(C.byref(ad), x, x, x, None, 0, x) == E
+    assert b"1024" in lib.rgo_last_error()
