@@ -666,6 +666,26 @@ def bench_chunked(rgo, wl, rank, world, args, peaks, mask_ms_l):
     return out
 
 
+def bench_tp_emulated(rgo, wl, world, steps=10):
+    """One rank's share of a tensor-parallel (tp = 2) Llama2-7B step (rgo_block_create_tp) on this
+    GPU: half the heads (and their compact mask), half the FFN, the two two-shot all-reduce
+    kernels at full size and the four host barriers of a step -- with the peer's buffers emulated
+    by local scratch (the all-reduce reads HBM instead of NVLink; no second GPU here)."""
+    import torch
+    out = {"config": "Llama2-7B block, tp=2, rank 0 of an emulated pair (peer buffers local, barriers no-op): "
+                     "heads 16, FFN 5504, mask 128 MiB per rank",
+           "modes_ms": {}}
+    for mode in ("serial_fused", "in_gemm", "no_rng"):
+        blk = rgo.TPBlock(wl, mode, seed=42, emulate=(2, 0))
+        out["modes_ms"][mode] = round(event_ms(blk.step, steps, world, warm=3), 4)
+        blk.close()
+        del blk
+        torch.cuda.empty_cache()
+    m = out["modes_ms"]
+    out["speedup_vs_fused"] = round(m["serial_fused"] / m["in_gemm"], 4)
+    return out
+
+
 def bench_gemms(rgo, wl, world, peaks):
     import torch
     f8 = torch.float8_e4m3fn
@@ -947,6 +967,12 @@ def bench_block(args, rank, world):
         # (B1 nH32 SQ32K, C = 8: 1 GiB live instead of 4 GiB), against the unchunked step.
         log("SQ-chunk pipeline")
         line["chunked_pipeline"] = bench_chunked(rgo, wl, rank, world, args, peaks, mask_ms)
+        if world == 1 and wl.ffn() % 256 == 0:
+            log("tensor-parallel rank (emulated pair)")
+            try:
+                line["tp2_rank_emulated"] = bench_tp_emulated(rgo, wl, world)
+            except Exception as e:  # an extra: never lose the main line over it
+                line["tp2_rank_emulated"] = {"error": str(e)[:200]}
         log("attention fwd+bwd")
         line["attention_fwd_bwd"] = bench_attention_bwd(rgo, rank, world, peaks)
         log("flash-attn library baseline")

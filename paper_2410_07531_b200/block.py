@@ -187,11 +187,18 @@ class TPBlock:
     `group` (torch.distributed) only carries the IPC handles and the step's barriers."""
 
     def __init__(self, cfg: WorkloadConfig, mode: str = "in_gemm", seed: int = 42, base_offset: int = 0,
-                 group=None, device="cuda", weights=None, rng_launch=(0, 0, 0)):
+                 group=None, device="cuda", weights=None, rng_launch=(0, 0, 0), emulate=None):
+        """emulate=(size, rank): no process group -- the other ranks' buffers are local scratch
+        tensors and the barriers are no-ops: times one rank's share of a TP step on one GPU (its
+        GEMMs, attention, mask and all-reduce kernels at full size; the peer data is stale, so
+        the outputs mean nothing)."""
         import torch
         import torch.distributed as dist
         self.group = group
-        size, rank = dist.get_world_size(group), dist.get_rank(group)
+        if emulate is not None:
+            size, rank = emulate
+        else:
+            size, rank = dist.get_world_size(group), dist.get_rank(group)
         self.size, self.rank, self.cfg, self.mode = size, rank, cfg, mode
         B, S, H, D = cfg.batch, cfg.seq, cfg.heads, cfg.head_dim
         d, F = H * D, cfg.ffn()
@@ -218,8 +225,22 @@ class TPBlock:
         self.mask = torch.zeros(B * Hl * S * S // 8, dtype=torch.uint8, device=dev)
         self.counter = torch.zeros(1, dtype=torch.int64, device=dev)
         torch.cuda.synchronize()
-        # exchange the peer buffers (CUDA IPC handles through the group)
         L = _lib.lib()
+        self._opened = {}
+        if emulate is not None:
+            tp = _lib.block_tp()
+            tp.size, tp.rank = size, rank
+            self._scratch = []
+            for r in range(size):
+                for arr, own in ((tp.peer_part, self.part), (tp.peer_y1, self.y1), (tp.peer_x, self.x)):
+                    if r == rank:
+                        arr[r] = own.data_ptr()
+                    else:
+                        self._scratch.append(torch.zeros_like(own))
+                        arr[r] = self._scratch[-1].data_ptr()
+            self._finish(cfg, tp, mode, seed, base_offset, rng_launch, lambda _ctx: None)
+            return
+        # exchange the peer buffers (CUDA IPC handles through the group)
         mine = []
         for t in (self.part, self.y1, self.x):
             h, off = (C.c_uint8 * 64)(), C.c_uint64()
@@ -227,7 +248,7 @@ class TPBlock:
             mine.append((bytes(h), off.value))
         allh = [None] * size
         dist.all_gather_object(allh, mine, group=group)
-        self._opened = {}  # IPC handle -> mapped allocation base (one mapping per peer allocation)
+        # IPC handle -> mapped allocation base (one mapping per peer allocation)
         tp = _lib.block_tp()
         tp.size, tp.rank = size, rank
         for r in range(size):
@@ -241,6 +262,12 @@ class TPBlock:
                     _lib.check(L.rgo_ipc_open((C.c_uint8 * 64).from_buffer_copy(handle), C.byref(p)))
                     self._opened[handle] = p.value
                 arr[r] = self._opened[handle] + off
+        self._finish(cfg, tp, mode, seed, base_offset, rng_launch, lambda _ctx: dist.barrier(group=group))
+
+    def _finish(self, cfg, tp, mode, seed, base_offset, rng_launch, barrier):
+        L = _lib.lib()
+        B, S, H, D = cfg.batch, cfg.seq, cfg.heads, cfg.head_dim
+        d, F = H * D, cfg.ffn()
         self.tp = tp
         desc = _lib.block_desc()
         desc.batch, desc.seq, desc.heads, desc.head_dim, desc.ffn = B, S, H, D, F
@@ -263,7 +290,7 @@ class TPBlock:
         handle = C.c_void_p()
         _lib.check(L.rgo_block_create_tp(desc, self._bufs, C.byref(tp), MODES[mode], C.byref(handle)))
         self.handle = handle
-        self._barrier = _lib.BARRIER_FN(lambda _ctx: dist.barrier(group=group))
+        self._barrier = _lib.BARRIER_FN(barrier)
 
     def step(self, stream=None) -> int:
         import torch
