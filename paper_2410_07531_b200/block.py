@@ -290,13 +290,24 @@ class TPBlock:
         handle = C.c_void_p()
         _lib.check(L.rgo_block_create_tp(desc, self._bufs, C.byref(tp), MODES[mode], C.byref(handle)))
         self.handle = handle
-        self._barrier = _lib.BARRIER_FN(barrier)
+        self._barrier_error = None
+
+        def guarded(ctx):  # an exception cannot cross the C ABI: record it, raise after the step
+            try:
+                barrier(ctx)
+            except BaseException as e:  # noqa: BLE001
+                if self._barrier_error is None:
+                    self._barrier_error = e
+        self._barrier = _lib.BARRIER_FN(guarded)
 
     def step(self, stream=None) -> int:
         import torch
         s = (stream or torch.cuda.current_stream()).cuda_stream
         n = C.c_int32()
         _lib.check(_lib.lib().rgo_block_step_tp(self.handle, s, self._barrier, None, C.byref(n)))
+        if self._barrier_error is not None:
+            e, self._barrier_error = self._barrier_error, None
+            raise RuntimeError("tensor-parallel step: a rank barrier failed, the step's result is invalid") from e
         return n.value
 
     def last_timings3(self):
