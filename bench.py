@@ -1073,13 +1073,16 @@ def main():
             return
         cfg = dict(L, rounds=args.rounds)
         steps = max(1, min(args.steps, 3))  # each step is a ~10 s CPU sample
+        warm = min(max(args.warmup, 0), 1)   # one untimed sample warms caches / thread pool
+        for _ in range(warm):
+            cpu_reference_block(cfg)
         vals = [cpu_reference_block(cfg) for _ in range(steps)]
         v = sum(x["value"] for x in vals) / len(vals)
         b = vals[-1]
         suite = cpu_baseline_suite(args.rounds)
         print(json.dumps({
             "metric": "llama2_block_ms", "value": round(v, 1), "unit": "ms", "n_gpus": 0, "impl": "reference",
-            "steps": steps, "warmup": 0, "higher_is_better": False, "scaling": "weak",
+            "steps": steps, "warmup": warm, "higher_is_better": False, "scaling": "weak",
             "config": {"workload": "Llama2-7B block (reference CPU path: generate_mask + attention_dropout_fused; "
                                    "no GEMMs in the reference)", "global_batch": cfg["batch"], "seq_len": cfg["seq"]},
             "cpu_baseline": {"value": round(v, 1), "unit": "ms", "cores": b["cores"], "kind": b["kind"],
