@@ -34,12 +34,12 @@ def _free_port():
     return p
 
 
-def _cfg(rgo):
-    return rgo.WorkloadConfig(batch=2, seq=512, heads=4, head_dim=128, ffn_dim=512, gated=True, keep_prob=0.9,
+def _cfg(rgo, gated=True):
+    return rgo.WorkloadConfig(batch=2, seq=512, heads=4, head_dim=128, ffn_dim=512, gated=gated, keep_prob=0.9,
                               philox_rounds=10)
 
 
-def _tp_worker(rank, world, port, q):
+def _tp_worker(rank, world, port, q, gated):
     import torch
     import torch.distributed as dist
     sys.path.insert(0, ROOT)
@@ -50,7 +50,7 @@ def _tp_worker(rank, world, port, q):
     try:
         out = {}
         for mode in ("in_gemm", "streams", "serial_fused"):
-            b = rgo.TPBlock(_cfg(rgo), mode, seed=42, base_offset=1000)
+            b = rgo.TPBlock(_cfg(rgo, gated), mode, seed=42, base_offset=1000)
             for _ in range(2):
                 b.step()
             torch.cuda.synchronize()
@@ -63,20 +63,21 @@ def _tp_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_tp2_block_matches_unsharded(rgo, cuda):
+@pytest.mark.parametrize("gated", [True, False])
+def test_tp2_block_matches_unsharded(rgo, cuda, gated):
     import torch
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_tp_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_tp_worker, args=(r, 2, port, q, gated)) for r in range(2)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=600) for _ in range(2))
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
-    cfg = _cfg(rgo)
+    cfg = _cfg(rgo, gated)
     ref = rgo.Block(cfg, "in_gemm", seed=42, base_offset=1000)
     ref.step()
     torch.cuda.synchronize()
@@ -101,9 +102,10 @@ def test_tp2_block_matches_unsharded(rgo, cuda):
     emul = {"y1": q8(parts[0] + parts[1]).cpu().numpy()}
 
     def emul_h(t, y1):
-        w1 = Ws[t]["w1"].float().view(-1, 2, 128, d)
-        acc = a_d * torch.from_numpy(y1).to(dev) @ w1.reshape(-1, d).T
-        acc = acc.view(M, -1, 2, 128)
+        acc = a_d * torch.from_numpy(y1).to(dev) @ Ws[t]["w1"].float().T
+        if not gated:  # GELU (tanh form, as the epilogue computes it)
+            return q8(torch.nn.functional.gelu(acc, approximate="tanh") * 2.0).cpu().numpy()
+        acc = acc.view(M, -1, 2, 128)  # SwiGLU row tiles [128 gate | 128 up]
         g, u = acc[:, :, 0, :].reshape(M, -1), acc[:, :, 1, :].reshape(M, -1)
         return q8(torch.nn.functional.silu(g) * u * 2.0).cpu().numpy()
 
