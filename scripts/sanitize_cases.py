@@ -1,6 +1,9 @@
 """Small invocation of every kernel, for compute-sanitizer (scripts/sanitize.sh):
-K1, K2 (bf16 + FP8 with each epilogue), K4 (12 RNG warps) + queue tail, K5/K6,
-K7 (head dim 64 and 128, bits and Philox), and one in-GEMM block step."""
+K1, K2 (bf16 + FP8 with each epilogue), K4 (12 RNG warps) + queue tail, K5/K6
+(mask bits by TMA), K7 (head dim 64 and 128, bits and Philox), K5g (head_dim 160),
+an in-GEMM and a streams block step, an SQ-chunked step, and one rank of a
+tensor-parallel step (emulated pair: the two-shot all-reduce kernels, the head-window
+mask)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -33,8 +36,23 @@ for D in (64, 128):
         rgo.attn_bwd(q, k, v, o, do, lse, **kw)                        # K7
 cfg = rgo.WorkloadConfig(batch=1, seq=256, heads=2, head_dim=128, ffn_dim=256, gated=True, keep_prob=0.9,
                          philox_rounds=10)
-blk = rgo.Block(cfg, "in_gemm", seed=42, use_graph=False)
+for mode in ("in_gemm", "streams"):
+    blk = rgo.Block(cfg, mode, seed=42, use_graph=False)
+    blk.step()
+    torch.cuda.synchronize()
+    blk.close()
+blk = rgo.Block(rgo.WorkloadConfig(batch=1, seq=512, heads=2, head_dim=128, ffn_dim=256, gated=True, keep_prob=0.9,
+                                   philox_rounds=10), "in_gemm", seed=42, use_graph=False, chunks=2)
 blk.step()
 torch.cuda.synchronize()
 blk.close()
+tcfg = rgo.WorkloadConfig(batch=1, seq=256, heads=4, head_dim=128, ffn_dim=512, gated=True, keep_prob=0.9,
+                          philox_rounds=10)
+for mode in ("in_gemm", "serial_fused"):
+    tb = rgo.TPBlock(tcfg, mode, seed=42, emulate=(2, 1))
+    tb.step()
+    torch.cuda.synchronize()
+    tb.close()
+inp = rgo.random_attention_input(2, 64, 160, 5)                        # K5g
+rgo.attention_dropout_fused(inp, 42, 0.9, 10)
 print("sanitize cases done")
