@@ -789,6 +789,8 @@ static cudaError_t enqueue_tp_segment(Block& b, int seg, int* launches) {
     return cudaSuccess;
 }
 
+int block_tp_size(const Block* b) { return b->cfg.tp_size; }
+
 cudaError_t block_step_tp(Block* b, cudaStream_t stream, TpBarrier barrier, void* ctx, int* launches) {
     if (b->cfg.tp_size < 2 || !barrier) return cudaErrorInvalidValue;
     cudaError_t e;

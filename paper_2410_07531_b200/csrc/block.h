@@ -79,6 +79,7 @@ cudaError_t block_step(Block* b, cudaStream_t stream, int* launches);
 // quant + Proj | reduce(Proj) | gather + FFN1 + FFN2 | reduce(FFN2) | gather + QKV +
 // attention.  Every rank must call it once per step.
 cudaError_t block_step_tp(Block* b, cudaStream_t stream, TpBarrier barrier, void* ctx, int* launches);
+int block_tp_size(const Block* b);
 // Device time of the last step's phases: [0] GEMM window (quant + 4 GEMMs),
 // [1] attention (incl. the RNG join / tail), in ms.
 cudaError_t block_last_timings(Block* b, float* ms2);

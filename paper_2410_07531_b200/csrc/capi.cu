@@ -602,6 +602,8 @@ int rgo_block_create_tp(const rgo_block_desc* d, const rgo_block_buffers* b, con
 
 int rgo_block_step_tp(rgo_block* blk, rgo_stream_t stream, rgo_barrier_fn barrier, void* ctx, int32_t* launches) {
     if (!blk || !barrier) return fail(RGO_EINVAL, "rgo_block_step_tp: null argument");
+    if (rgo::block_tp_size(blk->impl) < 2)
+        return fail(RGO_EINVAL, "rgo_block_step_tp: not a tensor-parallel block (use rgo_block_step)");
     int n = 0;
     cudaError_t ce = rgo::block_step_tp(blk->impl, static_cast<cudaStream_t>(stream), barrier, ctx, &n);
     if (launches) *launches = n;
@@ -660,6 +662,8 @@ int rgo_ipc_close(void* d_base) {
 
 int rgo_block_step(rgo_block* blk, rgo_stream_t stream, int32_t* launches) {
     if (!blk) return fail(RGO_EINVAL, "rgo_block_step: null handle");
+    if (rgo::block_tp_size(blk->impl) > 1)
+        return fail(RGO_EINVAL, "rgo_block_step: a tensor-parallel block steps with rgo_block_step_tp");
     int n = 0;
     cudaError_t ce = rgo::block_step(blk->impl, static_cast<cudaStream_t>(stream), &n);
     if (launches) *launches = n;
