@@ -19,6 +19,7 @@ struct AttnParams {
     uint64_t bits_bytes;
     int bits_aligned;        // SQ % 128 == 0 and 16-byte aligned bits
     int mask_tma;            // MASK_BITS: keep-bit tiles arrive by TMA (bits_aligned, the kernel's tmM)
+    int o_tma;               // O leaves by TMA store (the kernel's tmO)
     uint32_t k0, k1;         // MASK_PHILOX: key
     uint64_t base_offset;
     uint32_t thr;            // threshold < 2^32

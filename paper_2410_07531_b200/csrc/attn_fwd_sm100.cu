@@ -57,6 +57,9 @@ constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
 #ifndef RGO_FWD_MASK_TMA
 #define RGO_FWD_MASK_TMA 1
 #endif
+#ifndef RGO_FWD_O_TMA
+#define RGO_FWD_O_TMA 1
+#endif
 #ifndef RGO_FWD_MSK_STAGES
 #define RGO_FWD_MSK_STAGES 4
 #endif
@@ -176,6 +179,10 @@ __device__ __forceinline__ float2 ex2_poly2(float x0, float x1) {
 #define RGO_POLY_EVERY 8
 #endif
 constexpr int POLY_EVERY = RGO_POLY_EVERY;
+
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
 // Mask-bits prefetch distance in KV tiles (MASK_BITS): the row loads are
 // 32 rows apart per warp; two tiles ahead measured 2-3 % faster than one at
 // B4 H32 SQ4096 and B1 H32 SQ2K/32K (three: no better; profiles/r02_fwd_experiments.md).
@@ -184,11 +191,33 @@ constexpr int POLY_EVERY = RGO_POLY_EVERY;
 #endif
 constexpr int MASK_AHEAD = RGO_FWD_MASK_AHEAD;
 
+#ifdef RGO_FWD_TIMING  // diagnostic builds only: per-CTA phase timestamps
+__device__ unsigned long long* g_fwd_dbg = nullptr;
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void dbg_mark(int slot) {
+    if (g_fwd_dbg) {
+        uint32_t sm;
+        asm("mov.u32 %0, %%smid;" : "=r"(sm));
+        g_fwd_dbg[blockIdx.x * 8 + slot] = gtimer();
+        if (slot == 0) g_fwd_dbg[blockIdx.x * 8 + 7] = sm;
+    }
+}
+#define RGO_DBG_MARK(cond, slot) \
+    if (cond) dbg_mark(slot)
+#else
+#define RGO_DBG_MARK(cond, slot)
+#endif
+
 template <int HD, int MODE, int R>
 __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ,
                                                               const __grid_constant__ CUtensorMap tmK,
                                                               const __grid_constant__ CUtensorMap tmV,
                                                               const __grid_constant__ CUtensorMap tmM,
+                                                              const __grid_constant__ CUtensorMap tmO,
                                                               const AttnParams p) {
     using SM = Smem<HD>;
     extern __shared__ uint8_t smem_raw[];
@@ -212,6 +241,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(const __grid_const
     static_assert((17 + 2 * MSK_STAGES) * 8 + 4 <= 256, "barrier area");
 
     const uint32_t warp = warp_id(), lane = lane_id();
+    RGO_DBG_MARK(threadIdx.x == 0, 0);
     const int pair = blockIdx.x % p.n_pairs;
     const int bh = blockIdx.x / p.n_pairs;
     const int hh = bh % p.H, bb = bh / p.H;
@@ -248,6 +278,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(const __grid_const
     const uint32_t tmem = *tmem_slot;
     constexpr int NCH = HD / 64;
     griddep_wait();  // launched as a programmatic dependent: the producers of Q/K/V and the mask are done
+    RGO_DBG_MARK(threadIdx.x == 0, 1);
 
     if (warp < 4) {  // ---------------------------------------------- control warpgroup
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(CTRL_REGS));
@@ -423,6 +454,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(const __grid_const
                 kw[0] = kw[1] = kw[2] = kw[3] = 0;
             }
             mbar_wait(smem_u32(&s_full[w]), j & 1);
+            RGO_DBG_MARK(j == 0 && warp == 4 && lane == 0, 2);
             tc_fence_after();
             uint32_t s[4][32];
 #pragma unroll
@@ -515,38 +547,79 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(const __grid_const
             if (lane == 0) mbar_arrive(smem_u32(&p_full[w]));
         }
         // ---------------- epilogue: O / (l * keep_prob) -> bf16 rows
+        RGO_DBG_MARK(warp == 4 && lane == 0, 3);
         mbar_wait(smem_u32(&o_done[w]), 0);
+        RGO_DBG_MARK(warp == 4 && lane == 0, 4);
         tc_fence_after();
         const float inv = 1.0f / (l * p.keep_prob);
-        __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(p.O) + bb * p.o_sb + hh * p.o_sh +
-                              static_cast<long long>(row_valid ? i : 0) * p.o_ss;
+        if (p.o_tma) {
+            // O -> bf16 rows staged in shared memory as the SW128 tile of the output tensor
+            // map (tile w reuses K ring stage w: every MMA has completed), then one TMA store
+            // per 64-column block: coalesced 128-byte rows instead of 32 rows x 16 bytes per
+            // warp store (the epilogue was ~3 us of a ~56 us CTA at the Llama2-7B shape)
+            uint8_t* stg = sK + w * SM::TILE;
 #pragma unroll 1
-        for (int c = 0; c < HD / 32; ++c) {
-            uint32_t o[32];
-            tmem_ld32(tO + c * 32, o);
-            tmem_ld_wait_regs(o);
-            uint32_t packed[16];
+            for (int c = 0; c < HD / 32; ++c) {
+                uint32_t o[32];
+                tmem_ld32(tO + c * 32, o);
+                tmem_ld_wait_regs(o);
+                uint32_t packed[16];
 #pragma unroll
-            for (int e = 0; e < 16; ++e) {
-                __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(o[2 * e]) * inv, __uint_as_float(o[2 * e + 1]) * inv);
-                packed[e] = *reinterpret_cast<uint32_t*>(&h);
+                for (int e = 0; e < 16; ++e) {
+                    __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(o[2 * e]) * inv,
+                                                             __uint_as_float(o[2 * e + 1]) * inv);
+                    packed[e] = *reinterpret_cast<uint32_t*>(&h);
+                }
+                uint8_t* line = stg + (c >> 1) * SM::CHUNK + row * 128;
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    const uint32_t unit = static_cast<uint32_t>((c & 1) * 4 + v) ^ static_cast<uint32_t>(row & 7);
+                    *reinterpret_cast<uint4*>(line + unit * 16) =
+                        make_uint4(packed[4 * v], packed[4 * v + 1], packed[4 * v + 2], packed[4 * v + 3]);
+                }
             }
-            if (row_valid) {
-                uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+            fence_proxy_async_smem();
+            named_bar_sync(1 + w, 128);
+            if (warp == 4 + 4 * w && lane == 0) {
+                for (int cb = 0; cb < HD / 64; ++cb)
+                    tma_store_4d(&tmO, smem_u32(stg + cb * SM::CHUNK), cb * 64, q0 + w * BQ, hh, bb);
+                bulk_group_commit();
+                bulk_group_wait_read0();  // the staging smem is read before the CTA may exit
+            }
+        } else {
+            __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(p.O) + bb * p.o_sb + hh * p.o_sh +
+                                  static_cast<long long>(row_valid ? i : 0) * p.o_ss;
+#pragma unroll 1
+            for (int c = 0; c < HD / 32; ++c) {
+                uint32_t o[32];
+                tmem_ld32(tO + c * 32, o);
+                tmem_ld_wait_regs(o);
+                uint32_t packed[16];
 #pragma unroll
-                for (int v = 0; v < 4; ++v)
-                    dst[v] = make_uint4(packed[4 * v], packed[4 * v + 1], packed[4 * v + 2], packed[4 * v + 3]);
+                for (int e = 0; e < 16; ++e) {
+                    __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(o[2 * e]) * inv,
+                                                             __uint_as_float(o[2 * e + 1]) * inv);
+                    packed[e] = *reinterpret_cast<uint32_t*>(&h);
+                }
+                if (row_valid) {
+                    uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+                    for (int v = 0; v < 4; ++v)
+                        dst[v] = make_uint4(packed[4 * v], packed[4 * v + 1], packed[4 * v + 2], packed[4 * v + 3]);
+                }
             }
         }
         if (p.lse && row_valid) p.lse[slice * p.S + p.q_row0 + i] = (m + __log2f(l)) * 0.6931471805599453f;
+        RGO_DBG_MARK(warp == 4 && lane == 0, 5);
     }
     __syncthreads();
+    RGO_DBG_MARK(threadIdx.x == 0, 6);
     if (warp == 1) tmem_dealloc<TMEM_COLS>(tmem);
 }
 
 template <int HD, int MODE, int R>
 static cudaError_t launch_t(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v, const CUtensorMap& m,
-                            const AttnParams& p, cudaStream_t s, bool pdl) {
+                            const CUtensorMap& o, const AttnParams& p, cudaStream_t s, bool pdl) {
     auto kern = attn_fwd_kernel<HD, MODE, R>;
     if (cudaError_t e = rgo::ensure_dyn_smem(reinterpret_cast<const void*>(kern), Smem<HD>::BYTES); e != cudaSuccess)
         return e;
@@ -561,10 +634,16 @@ static cudaError_t launch_t(const CUtensorMap& q, const CUtensorMap& k, const CU
     cfg.stream = s;
     cfg.attrs = at;
     cfg.numAttrs = pdl ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, kern, q, k, v, m, p);
+    return cudaLaunchKernelEx(&cfg, kern, q, k, v, m, o, p);
 }
 
 }  // namespace rgo_attn
+
+#ifdef RGO_FWD_TIMING
+extern "C" int rgo_debug_fwd_timing(unsigned long long* d_buf) {  // diagnostic builds only
+    return cudaMemcpyToSymbol(rgo_attn::g_fwd_dbg, &d_buf, sizeof(d_buf)) == cudaSuccess ? 0 : 2;
+}
+#endif
 
 namespace rgo {
 
@@ -623,8 +702,17 @@ cudaError_t launch_attn_fwd(const AttnJob& j, cudaStream_t s) {
         p.mask_tma = make_tmap(&tm, j.bits, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, dims, strides, box,
                                CU_TENSOR_MAP_SWIZZLE_NONE) ? 1 : 0;
     }
+    // O by TMA store (16-byte aligned base and strides: the tensor map's requirement)
+    CUtensorMap to;
+    std::memset(&to, 0, sizeof(to));
+    p.o_tma = 0;
+    if (RGO_FWD_O_TMA && (reinterpret_cast<uintptr_t>(j.o.ptr) & 15) == 0 && j.o.ss % 8 == 0 && j.o.sh % 8 == 0 &&
+        j.o.sb % 8 == 0) {
+        const AttnTensor ov{j.o.ptr, j.o.sb, j.o.sh, j.o.ss};
+        p.o_tma = tmap_qkv(&to, ov, j.B, j.H, Sq, j.HD) ? 1 : 0;
+    }
 #define RGO_A(HDV, MODEV, RV) \
-    if (j.HD == HDV && mode == MODEV) return launch_t<HDV, MODEV, RV>(tq, tk, tv, tm, p, s, j.pdl);
+    if (j.HD == HDV && mode == MODEV) return launch_t<HDV, MODEV, RV>(tq, tk, tv, tm, to, p, s, j.pdl);
     RGO_A(128, MASK_NONE, 0)
     RGO_A(64, MASK_NONE, 0)
     RGO_A(128, MASK_BITS, 0)
