@@ -20,6 +20,7 @@ struct AttnParams {
     int bits_aligned;        // SQ % 128 == 0 and 16-byte aligned bits
     int mask_tma;            // MASK_BITS: keep-bit tiles arrive by TMA (bits_aligned, the kernel's tmM)
     int o_tma;               // O leaves by TMA store (the kernel's tmO)
+    int resident;            // CTAs resident at once (SMs): the Q prefetch's next CTA = blockIdx + resident
     uint32_t k0, k1;         // MASK_PHILOX: key
     uint64_t base_offset;
     uint32_t thr;            // threshold < 2^32

@@ -57,6 +57,9 @@ constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
 #ifndef RGO_FWD_MASK_TMA
 #define RGO_FWD_MASK_TMA 1
 #endif
+#ifndef RGO_FWD_Q_PREFETCH
+#define RGO_FWD_Q_PREFETCH 1
+#endif
 #ifndef RGO_FWD_O_TMA
 #define RGO_FWD_O_TMA 1
 #endif
@@ -331,6 +334,19 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(const __grid_const
                 if (++vs == KV_STAGES) { vs = 0; vph ^= 1; }
                 if (mtma && j + MSK_STAGES - 1 < n_kv) load_mask(j + MSK_STAGES - 1);
             }
+            // Warm L2 for the CTA that will most likely take this SM next (CTAs are dispatched
+            // in index order, one per SM): its Q tiles are read by no other CTA, so its
+            // pipeline fill would otherwise start with an HBM round trip.
+            if (RGO_FWD_Q_PREFETCH && elect_one()) {
+                const int nb = blockIdx.x + p.resident;
+                if (p.resident > 0 && nb < static_cast<int>(gridDim.x)) {
+                    const int npair = nb % p.n_pairs, nbh = nb / p.n_pairs;
+                    for (int w = 0; w < 2; ++w)
+                        for (int c = 0; c < NCH; ++c)
+                            tma_prefetch_l2_4d(&tmQ, c * 64, npair * 2 * BQ + w * BQ, nbh % p.H, nbh / p.H);
+                }
+            }
+            __syncwarp();
         } else if (warp == 1) {  // MMA issuer (whole warp loops, one lane issues)
             constexpr uint32_t IDESC_S = idesc_make(1, 1, BQ, BKV, 0, 0);
             constexpr uint32_t IDESC_O = idesc_make(1, 1, BQ, HD, 0, 1);  // V is MN-major
@@ -671,6 +687,7 @@ cudaError_t launch_attn_fwd(const AttnJob& j, cudaStream_t s) {
     p.bits_rows = j.bits_rows > 0 ? j.bits_rows : j.S;
     if (p.bits_rows != j.S && p.bits_rows != Sq) return cudaErrorInvalidValue;
     p.n_pairs = (Sq + 2 * BQ - 1) / (2 * BQ);
+    p.resident = rgo::num_sms();  // one CTA per SM (shared memory, 512 TMEM columns)
     p.scale_log2 = j.scale * 1.4426950408889634f;
     p.keep_prob = j.mode == MASK_NONE ? 1.0f : j.keep_prob;
     p.bits = j.bits;
