@@ -91,6 +91,7 @@ struct Params {
     long long k_sb, k_sh, k_ss;  // dK strides (elements)
     long long v_sb, v_sh, v_ss;  // dV strides
     int mask_tma;                // v2, MASK_BITS: the keep-bit tile arrives by TMA with Q (SQ % 128 == 0)
+    int dkv_tma;                 // v2: dK/dV leave by TMA store (the kernel's tmdK/tmdV)
 };
 
 // Blocked dQ accumulator: per (slice, query tile) HD/32 column chunks of 8
@@ -723,6 +724,9 @@ constexpr int DQ_BUFS = KT_TMEM ? 1 : 2;  // dQ^T accumulators in TMEM
 #define RGO_BWD_MSK_STAGES 2
 #endif
 constexpr int MSK_STAGES = RGO_BWD_MSK_STAGES;
+#ifndef RGO_BWD_DKV_TMA
+#define RGO_BWD_DKV_TMA 1
+#endif
 
 struct Smem2 {
     static constexpr int KCHUNK = 128 * 128;  // K/V: 128 rows x 128 B per 64-dim chunk
@@ -824,6 +828,8 @@ __global__ void __launch_bounds__(THREADS, 1) bwd_main2_kernel(const __grid_cons
                                                                const __grid_constant__ CUtensorMap tmV,
                                                                const __grid_constant__ CUtensorMap tmdO,
                                                                const __grid_constant__ CUtensorMap tmM,
+                                                               const __grid_constant__ CUtensorMap tmdK,
+                                                               const __grid_constant__ CUtensorMap tmdV,
                                                                const Params p) {
     using SM = Smem2;
     constexpr int HD = 128;
@@ -1151,6 +1157,41 @@ __global__ void __launch_bounds__(THREADS, 1) bwd_main2_kernel(const __grid_cons
         // ---- epilogue: dV = acc / keep_prob, dK = acc * scale; dims [64h, 64h+64)
         mbar_wait(smem_u32(acc_full), 0);
         tc_fence_after();
+        if (p.dkv_tma) {
+            // staged as the SW128 tiles of the output tensor maps in the K (dV) and V (dK)
+            // buffers -- every MMA has completed -- then one TMA store per tensor and dims
+            // half: coalesced 128-byte rows instead of 32 key rows x 16 bytes per warp store
+#pragma unroll 1
+            for (int which = 0; which < 2; ++which) {
+                const uint32_t tacc = tmem + lane_base + 256 + which * HD;
+                const float mul = which == 0 ? p.inv_keep : p.scale;
+                uint8_t* line = (which == 0 ? sK : sV) + h * SM::KCHUNK + r * 128;
+#pragma unroll 1
+                for (int c = 0; c < 2; ++c) {
+                    uint32_t o[32];
+                    tmem_ld32(tacc + h * 64 + 32 * c, o);
+                    tmem_ld_wait_regs(o);
+                    uint32_t pk[16];
+#pragma unroll
+                    for (int e = 0; e < 16; ++e)
+                        pk[e] = pack_bf16(__uint_as_float(o[2 * e]) * mul, __uint_as_float(o[2 * e + 1]) * mul);
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) {
+                        const uint32_t unit = static_cast<uint32_t>(4 * c + v) ^ static_cast<uint32_t>(r & 7);
+                        *reinterpret_cast<uint4*>(line + unit * 16) =
+                            make_uint4(pk[4 * v], pk[4 * v + 1], pk[4 * v + 2], pk[4 * v + 3]);
+                    }
+                }
+            }
+            fence_proxy_async_smem();
+            named_bar_sync(2 + h, 128);
+            if (qw == 0 && lane == 0) {
+                tma_store_4d(&tmdV, smem_u32(sK + h * SM::KCHUNK), h * 64, kv0, hh, bb);
+                tma_store_4d(&tmdK, smem_u32(sV + h * SM::KCHUNK), h * 64, kv0, hh, bb);
+                bulk_group_commit();
+                bulk_group_wait_read0();  // the staging smem is read before the CTA may exit
+            }
+        } else {
         const int key = kv0 + r;
         __nv_bfloat16* dv_row = static_cast<__nv_bfloat16*>(p.dV) + bb * p.v_sb + hh * p.v_sh +
                                 static_cast<long long>(key_valid ? key : 0) * p.v_ss;
@@ -1177,6 +1218,7 @@ __global__ void __launch_bounds__(THREADS, 1) bwd_main2_kernel(const __grid_cons
                     for (int v = 0; v < 4; ++v) d4[v] = make_uint4(pk[4 * v], pk[4 * v + 1], pk[4 * v + 2], pk[4 * v + 3]);
                 }
             }
+        }
         }
     } else if (warp >= 12) {  // ------------------------------------------------- dQ drain
         // thread = head dim (TMEM lane 32*qw + lane), 64 query values per tile
@@ -1254,11 +1296,12 @@ __global__ void __launch_bounds__(THREADS, 1) bwd_main2_kernel(const __grid_cons
 
 template <int MODE, int R>
 static cudaError_t launch_main2(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
-                                const CUtensorMap& dO, const CUtensorMap& m, const Params& p, cudaStream_t s) {
+                                const CUtensorMap& dO, const CUtensorMap& m, const CUtensorMap& dk,
+                                const CUtensorMap& dv, const Params& p, cudaStream_t s) {
     auto kern = bwd_main2_kernel<MODE, R>;
     if (cudaError_t e = rgo::ensure_dyn_smem(reinterpret_cast<const void*>(kern), Smem2::ALLOC); e != cudaSuccess) return e;
     const unsigned grid = static_cast<unsigned>(p.B) * p.H * p.n_kt;
-    kern<<<grid, THREADS, Smem2::ALLOC, s>>>(q, k, v, dO, m, p);
+    kern<<<grid, THREADS, Smem2::ALLOC, s>>>(q, k, v, dO, m, dk, dv, p);
     return cudaGetLastError();
 }
 
@@ -1679,11 +1722,23 @@ static cudaError_t launch_attn_bwd2(const AttnBwdJob& j, cudaStream_t s) {
         p.mask_tma = make_tmap(&tm, j.bits, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, dims, strides, box,
                                CU_TENSOR_MAP_SWIZZLE_NONE) ? 1 : 0;
     }
-    if (mode == rgo_attn::MASK_NONE) e = launch_main2<rgo_attn::MASK_NONE, 0>(tq, tk, tv, tdo, tm, p, s);
-    else if (mode == rgo_attn::MASK_BITS) e = launch_main2<rgo_attn::MASK_BITS, 0>(tq, tk, tv, tdo, tm, p, s);
-    else if (j.rounds == 10) e = launch_main2<rgo_attn::MASK_PHILOX, 10>(tq, tk, tv, tdo, tm, p, s);
-    else if (j.rounds == 7) e = launch_main2<rgo_attn::MASK_PHILOX, 7>(tq, tk, tv, tdo, tm, p, s);
-    else e = launch_main2<rgo_attn::MASK_PHILOX, 0>(tq, tk, tv, tdo, tm, p, s);
+    // dK/dV by TMA store (16-byte aligned bases and strides)
+    CUtensorMap tdk, tdv;
+    std::memset(&tdk, 0, sizeof(tdk));
+    std::memset(&tdv, 0, sizeof(tdv));
+    auto al16 = [](const AttnOut& t) {
+        return (reinterpret_cast<uintptr_t>(t.ptr) & 15) == 0 && t.ss % 8 == 0 && t.sh % 8 == 0 && t.sb % 8 == 0;
+    };
+    p.dkv_tma = RGO_BWD_DKV_TMA && al16(j.dk) && al16(j.dv) &&
+                tmap4(&tdk, AttnTensor{j.dk.ptr, j.dk.sb, j.dk.sh, j.dk.ss}, j.B, j.H, j.S, j.HD) &&
+                tmap4(&tdv, AttnTensor{j.dv.ptr, j.dv.sb, j.dv.sh, j.dv.ss}, j.B, j.H, j.S, j.HD);
+#define RGO_M2(MODEV, RV) launch_main2<MODEV, RV>(tq, tk, tv, tdo, tm, tdk, tdv, p, s)
+    if (mode == rgo_attn::MASK_NONE) e = RGO_M2(rgo_attn::MASK_NONE, 0);
+    else if (mode == rgo_attn::MASK_BITS) e = RGO_M2(rgo_attn::MASK_BITS, 0);
+    else if (j.rounds == 10) e = RGO_M2(rgo_attn::MASK_PHILOX, 10);
+    else if (j.rounds == 7) e = RGO_M2(rgo_attn::MASK_PHILOX, 7);
+    else e = RGO_M2(rgo_attn::MASK_PHILOX, 0);
+#undef RGO_M2
     if (e != cudaSuccess) return e;
     const uint64_t n = static_cast<uint64_t>(j.B) * j.H * n_qt * 256;
     bwd_dq2_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
