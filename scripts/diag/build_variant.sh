@@ -1,5 +1,5 @@
 #!/bin/bash
-# Build an alternative librgo_b200.so with extra nvcc flags into scripts/diag/libs/NAME.so
+# Build an alternative librgo_b200.so with extra nvcc flags into ablibs/NAME.so (repo root; remove it after the A/B run)
 # (for scripts/diag/ab_libs.sh):  scripts/diag/build_variant.sh NAME "-DRGO_POLY_EVERY=0" [files...]
 # With files listed (e.g. attn_fwd_sm100.cu), the objects of the in-tree build are reused and
 # only those units are recompiled with the extra flags.
@@ -13,5 +13,5 @@ if [ $# -gt 0 ]; then
 else
   rm -rf $T/pkg/csrc/build
 fi
-mkdir -p $ROOT/scripts/diag/libs
-make -s -j16 -C $T/pkg/csrc NVFLAGS="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -I$T/include -I. --expt-relaxed-constexpr $FLAGS" OUT=$ROOT/scripts/diag/libs/$NAME.so
+mkdir -p $ROOT/ablibs
+make -s -j16 -C $T/pkg/csrc NVFLAGS="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -I$T/include -I. --expt-relaxed-constexpr $FLAGS" OUT=$ROOT/ablibs/$NAME.so
