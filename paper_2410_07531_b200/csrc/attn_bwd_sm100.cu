@@ -1189,7 +1189,7 @@ __global__ void __launch_bounds__(THREADS, 1) bwd_main2_kernel(const __grid_cons
                 tma_store_4d(&tmdV, smem_u32(sK + h * SM::KCHUNK), h * 64, kv0, hh, bb);
                 tma_store_4d(&tmdK, smem_u32(sV + h * SM::KCHUNK), h * 64, kv0, hh, bb);
                 bulk_group_commit();
-                bulk_group_wait_read0();  // the staging smem is read before the CTA may exit
+                bulk_group_wait_all();  // complete before the CTA exits (see K5's O store)
             }
         } else {
         const int key = kv0 + r;

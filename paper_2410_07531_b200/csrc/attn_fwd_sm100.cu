@@ -600,7 +600,10 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(const __grid_const
                 for (int cb = 0; cb < HD / 64; ++cb)
                     tma_store_4d(&tmO, smem_u32(stg + cb * SM::CHUNK), cb * 64, q0 + w * BQ, hh, bb);
                 bulk_group_commit();
-                bulk_group_wait_read0();  // the staging smem is read before the CTA may exit
+                // the store complete (not only its read of the staging smem) before the CTA
+                // exits: with only the read waited for, back-to-back eager block steps with
+                // programmatic dependent launch hung (scripts/diag/pdl_stress.py, streams mode)
+                bulk_group_wait_all();
             }
         } else {
             __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(p.O) + bb * p.o_sb + hh * p.o_sh +

@@ -49,6 +49,7 @@ __device__ __forceinline__ void bulk_group_commit() { asm volatile("cp.async.bul
 __device__ __forceinline__ void bulk_group_wait_read0() {
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
+__device__ __forceinline__ void bulk_group_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
