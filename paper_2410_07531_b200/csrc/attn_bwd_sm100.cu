@@ -754,58 +754,72 @@ __host__ __device__ __forceinline__ uint64_t dq2_tile_base(uint64_t slice, int n
     return (slice * n_qt + qt) * static_cast<uint64_t>(BQ2) * 128;
 }
 
+// Row terms of the 64-query-tile backward: D = dO . O and -lse*log2(e) per query row
+// (padding rows: 0, -inf).  Sixteen threads per row, each reading 16 bytes of O and dO,
+// so a warp reads two whole 256-byte rows per instruction; the fp32 dQ accumulator
+// (dq_zero float4s) is zeroed by the same grid, coalesced, instead of a separate memset.
 __global__ void bwd_prep2_kernel(const __nv_bfloat16* __restrict__ O, long long o_sb, long long o_sh, long long o_ss,
                                  const __nv_bfloat16* __restrict__ dO, long long d_sb, long long d_sh, long long d_ss,
                                  const float* __restrict__ lse, float* __restrict__ rows, int B, int H, int S,
-                                 int n_qt) {
+                                 int n_qt, float4* __restrict__ dq_zero, uint64_t n_zero) {
     const uint64_t padded = static_cast<uint64_t>(n_qt) * BQ2;
     const uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (t >= static_cast<uint64_t>(B) * H * padded) return;
-    const uint64_t slice = t / padded;
-    const int r = static_cast<int>(t - slice * padded);
+    const uint64_t n_thr = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t z = t; z < n_zero; z += n_thr) dq_zero[z] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const uint64_t row = t >> 4;
+    const int part = static_cast<int>(t & 15);
+    // rows is a multiple of 64, so only whole warps of the last block exit here and the
+    // 16-lane shuffles below always run with full warps
+    if (row >= static_cast<uint64_t>(B) * H * padded) return;
+    const uint64_t slice = row / padded;
+    const int r = static_cast<int>(row - slice * padded);
     const int qt = r / BQ2, rr = r % BQ2;
     const int bb = static_cast<int>(slice / H), hh = static_cast<int>(slice % H);
-    float d = 0.0f, nl = -INFINITY;
+    float d = 0.0f;
     if (r < S) {
-        const uint4* po = reinterpret_cast<const uint4*>(O + bb * o_sb + hh * o_sh + static_cast<long long>(r) * o_ss);
-        const uint4* pd = reinterpret_cast<const uint4*>(dO + bb * d_sb + hh * d_sh + static_cast<long long>(r) * d_ss);
-        float acc0 = 0.0f, acc1 = 0.0f;
-#pragma unroll 4
-        for (int c = 0; c < 16; ++c) {
-            const uint4 a = __ldg(po + c), b = __ldg(pd + c);
-            const uint32_t av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+        const uint4 a = __ldg(reinterpret_cast<const uint4*>(O + bb * o_sb + hh * o_sh + static_cast<long long>(r) * o_ss) + part);
+        const uint4 c = __ldg(reinterpret_cast<const uint4*>(dO + bb * d_sb + hh * d_sh + static_cast<long long>(r) * d_ss) + part);
+        const uint32_t av[4] = {a.x, a.y, a.z, a.w}, cv[4] = {c.x, c.y, c.z, c.w};
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                acc0 = fmaf(bf16_lo(av[e]), bf16_lo(bv[e]), acc0);
-                acc1 = fmaf(bf16_hi(av[e]), bf16_hi(bv[e]), acc1);
-            }
-        }
-        d = acc0 + acc1;
-        nl = -lse[slice * S + r] * 1.4426950408889634f;
+        for (int e = 0; e < 4; ++e) d = fmaf(bf16_hi(av[e]), bf16_hi(cv[e]), fmaf(bf16_lo(av[e]), bf16_lo(cv[e]), d));
     }
-    float* rw = rows + (slice * n_qt + qt) * (2 * BQ2);
-    rw[rr] = nl;
-    rw[BQ2 + rr] = d;
+#pragma unroll
+    for (int off = 8; off > 0; off >>= 1) d += __shfl_xor_sync(0xffffffffu, d, off);
+    if (part == 0) {
+        float* rw = rows + (slice * n_qt + qt) * (2 * BQ2);
+        rw[rr] = r < S ? -lse[slice * S + r] * 1.4426950408889634f : -INFINITY;
+        rw[BQ2 + rr] = d;
+    }
 }
 
-// thread = (slice, 64-query tile, group of 4 queries, 8 dims): 8 float4 reads
-// (128 contiguous bytes), 4 x 16-byte bf16 row writes.
-__global__ void bwd_dq2_kernel(const float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dQ, long long q_sb,
-                               long long q_sh, long long q_ss, int B, int H, int S, int n_qt, float scale) {
-    const uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const uint64_t per_tile = 16 * 16;  // query groups x dim groups
-    const uint64_t total = static_cast<uint64_t>(B) * H * n_qt * per_tile;
-    if (t >= total) return;
-    const uint64_t tile = t / per_tile;  // slice * n_qt + qt
-    const int rem = static_cast<int>(t - tile * per_tile);
-    const int dg = rem % 16, qg = rem / 16;
+// dQ = scale * accumulator -> bf16 rows.  One 256-thread block per (slice, 64-query tile):
+// the tile's blocked accumulator ([16 query groups][128 dims][4 queries] fp32, 32 KB) is read
+// with 512-byte coalesced float4 loads into shared memory (one float4 of padding every 8, so
+// the transposing reads below are conflict-free), then thread (query group, 8 dims) converts
+// its 4 x 8 values and writes 4 rows x 16 bytes (a half-warp writes whole 256-byte rows).
+__global__ void __launch_bounds__(256) bwd_dq2_kernel(const float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dQ,
+                                                      long long q_sb, long long q_sh, long long q_ss, int B, int H, int S,
+                                                      int n_qt, float scale) {
+    constexpr int N4 = BQ2 * 128 / 4;  // 2048 float4
+    __shared__ float4 tile_s[N4 + N4 / 8];
+    const uint64_t tile = blockIdx.x;  // slice * n_qt + qt
+    const float4* acc = reinterpret_cast<const float4*>(dq_acc + tile * BQ2 * 128);
+#pragma unroll
+    for (int k = 0; k < N4 / 256; ++k) {
+        const int i = threadIdx.x + 256 * k;
+        tile_s[i + (i >> 3)] = acc[i];
+    }
+    __syncthreads();
     const uint64_t slice = tile / n_qt;
     const int qt = static_cast<int>(tile - slice * n_qt);
-    const float4* acc = reinterpret_cast<const float4*>(dq_acc + tile * BQ2 * 128);
+    const int bb = static_cast<int>(slice / H), hh = static_cast<int>(slice % H);
+    const int dg = threadIdx.x & 15, qg = threadIdx.x >> 4;
     float4 v[8];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) v[e] = acc[qg * 128 + dg * 8 + e];
-    const int bb = static_cast<int>(slice / H), hh = static_cast<int>(slice % H);
+    for (int e = 0; e < 8; ++e) {
+        const int i = qg * 128 + dg * 8 + e;
+        v[e] = tile_s[i + (i >> 3)];
+    }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
         const int q = qt * BQ2 + qg * 4 + u;
@@ -1697,14 +1711,14 @@ static cudaError_t launch_attn_bwd2(const AttnBwdJob& j, cudaStream_t s) {
     const uint64_t rows = static_cast<uint64_t>(j.B) * j.H * n_qt * BQ2;
     float* dq_acc = static_cast<float*>(j.work);
     float* rowbuf = dq_acc + rows * j.HD;
-    cudaError_t e = cudaMemsetAsync(dq_acc, 0, rows * j.HD * sizeof(float), s);
-    if (e != cudaSuccess) return e;
-    {
+    cudaError_t e;
+    {  // row terms + zeroed fp32 dQ accumulator, one pass
         const unsigned threads = 256;
-        const unsigned grid = static_cast<unsigned>((rows + threads - 1) / threads);
+        const unsigned grid = static_cast<unsigned>((rows * 16 + threads - 1) / threads);
         bwd_prep2_kernel<<<grid, threads, 0, s>>>(static_cast<const __nv_bfloat16*>(j.o.ptr), j.o.sb, j.o.sh, j.o.ss,
                                                   static_cast<const __nv_bfloat16*>(j.dout.ptr), j.dout.sb, j.dout.sh,
-                                                  j.dout.ss, j.lse, rowbuf, j.B, j.H, j.S, n_qt);
+                                                  j.dout.ss, j.lse, rowbuf, j.B, j.H, j.S, n_qt,
+                                                  reinterpret_cast<float4*>(dq_acc), rows * j.HD / 4);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     Params p{};
@@ -1740,8 +1754,7 @@ static cudaError_t launch_attn_bwd2(const AttnBwdJob& j, cudaStream_t s) {
     else e = RGO_M2(rgo_attn::MASK_PHILOX, 0);
 #undef RGO_M2
     if (e != cudaSuccess) return e;
-    const uint64_t n = static_cast<uint64_t>(j.B) * j.H * n_qt * 256;
-    bwd_dq2_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
+    bwd_dq2_kernel<<<static_cast<unsigned>(static_cast<uint64_t>(j.B) * j.H * n_qt), 256, 0, s>>>(
         dq_acc, static_cast<__nv_bfloat16*>(j.dq.ptr), j.dq.sb, j.dq.sh, j.dq.ss, j.B, j.H, j.S, n_qt, j.scale);
     return cudaGetLastError();
 }
