@@ -63,6 +63,10 @@ constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
 #ifndef RGO_FWD_O_TMA
 #define RGO_FWD_O_TMA 1
 #endif
+#ifndef RGO_FWD_MASK_BOX_ROWS
+#define RGO_FWD_MASK_BOX_ROWS 256  // keep-bit rows per TMA box: both Q tiles (256) or one (128)
+#endif
+constexpr int MASK_BOX_ROWS = RGO_FWD_MASK_BOX_ROWS;
 #ifndef RGO_FWD_MSK_STAGES
 #define RGO_FWD_MSK_STAGES 4
 #endif
@@ -304,8 +308,13 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(const __grid_const
                 if (elect_one()) {
                     const uint32_t mb = smem_u32(&m_full[ms]);
                     mbar_arrive_expect_tx(mb, 2 * 2048);
-                    for (int w = 0; w < 2; ++w)
-                        tma_load_2d(smem_u32(smem + SM::MSK_OFF + (ms * 2 + w) * 2048), &tmM, mb, t * 16, mrow + w * BQ);
+                    if constexpr (MASK_BOX_ROWS == 2 * BQ) {  // both Q tiles' 256 rows in one box
+                        tma_load_2d(smem_u32(smem + SM::MSK_OFF + ms * 2 * 2048), &tmM, mb, t * 16, mrow);
+                    } else {
+                        for (int w = 0; w < 2; ++w)
+                            tma_load_2d(smem_u32(smem + SM::MSK_OFF + (ms * 2 + w) * 2048), &tmM, mb, t * 16,
+                                        mrow + w * BQ);
+                    }
                 }
                 __syncwarp();
             };
@@ -718,7 +727,7 @@ cudaError_t launch_attn_fwd(const AttnJob& j, cudaStream_t s) {
     if (RGO_FWD_MASK_TMA && mode == MASK_BITS && p.bits_aligned) {
         const uint64_t dims[2] = {static_cast<uint64_t>(j.S) / 8, static_cast<uint64_t>(j.B) * j.H * p.bits_rows};
         const uint64_t strides[1] = {static_cast<uint64_t>(j.S) / 8};
-        const uint32_t box[2] = {16, static_cast<uint32_t>(BQ)};
+        const uint32_t box[2] = {16, static_cast<uint32_t>(MASK_BOX_ROWS)};
         p.mask_tma = make_tmap(&tm, j.bits, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, dims, strides, box,
                                CU_TENSOR_MAP_SWIZZLE_NONE) ? 1 : 0;
     }
