@@ -724,6 +724,9 @@ constexpr int DQ_BUFS = KT_TMEM ? 1 : 2;  // dQ^T accumulators in TMEM
 #define RGO_BWD_MSK_STAGES 2
 #endif
 constexpr int MSK_STAGES = RGO_BWD_MSK_STAGES;
+// Each ring slot holds the keep bits of two consecutive query tiles (one 128-row TMA box;
+// tiles 2u and 2u+1 of the rotated order are always adjacent: the rotation is even).
+constexpr int MSK_SLOT = 2 * 1024;
 #ifndef RGO_BWD_DKV_TMA
 #define RGO_BWD_DKV_TMA 1
 #endif
@@ -742,7 +745,7 @@ struct Smem2 {
     static constexpr int STG_BYTES = 128 * BQ2 * 4;
     static constexpr int ROW_OFF = STG_OFF + 2 * STG_BYTES; // per stage: 64 -lse2, 64 D
     static constexpr int MSK_OFF = ROW_OFF + 2 * 512;        // per stage: 64 query rows x 16 B of keep bits
-    static constexpr int BAR_OFF = MSK_OFF + MSK_STAGES * 1024;
+    static constexpr int BAR_OFF = MSK_OFF + MSK_STAGES * MSK_SLOT;
     static constexpr int BYTES = BAR_OFF + 512;
     static constexpr int ALLOC = BYTES + 1023;
 };
@@ -927,20 +930,21 @@ __global__ void __launch_bounds__(THREADS, 1) bwd_main2_kernel(const __grid_cons
         __syncwarp();
         const float* rows = p.rows + slice * n_qt * (2 * BQ2);
         const bool mtma = MODE == MASK_BITS && p.mask_tma;
-        // keep bits of (64 query rows of tile t) x (this CTA's 128 keys) into ring slot t % MSK_STAGES
-        auto load_mask = [&](int t) {
-            const int ms = t % MSK_STAGES;
-            mbar_wait(smem_u32(&m_empty[ms]), ((t / MSK_STAGES) & 1) ^ 1);
+        // keep bits of (128 query rows of tiles 2u, 2u+1) x (this CTA's 128 keys) into slot u % MSK_STAGES
+        const int n_pairs_q = n_qt / 2;  // mask_tma implies SQ % 128 == 0: n_qt even
+        auto load_mask = [&](int u) {
+            const int ms = u % MSK_STAGES;
+            mbar_wait(smem_u32(&m_empty[ms]), ((u / MSK_STAGES) & 1) ^ 1);
             if (elect_one()) {
                 const uint32_t mb = smem_u32(&m_full[ms]);
-                mbar_arrive_expect_tx(mb, 1024);
-                tma_load_2d(smem_u32(smem + SM::MSK_OFF + ms * 1024), &tmM, mb, kv0 / 8,
-                            static_cast<int>(slice) * p.S + qtile(t) * BQ2);
+                mbar_arrive_expect_tx(mb, MSK_SLOT);
+                tma_load_2d(smem_u32(smem + SM::MSK_OFF + ms * MSK_SLOT), &tmM, mb, kv0 / 8,
+                            static_cast<int>(slice) * p.S + qtile(2 * u) * BQ2);
             }
             __syncwarp();
         };
         if (mtma)
-            for (int t = 0; t < MSK_STAGES - 1 && t < n_qt; ++t) load_mask(t);
+            for (int u = 0; u < MSK_STAGES - 1 && u < n_pairs_q; ++u) load_mask(u);
         for (int i = 0; i < n_qt; ++i) {
             const int st = i & 1;
             const uint32_t ph = (i >> 1) & 1;
@@ -954,7 +958,7 @@ __global__ void __launch_bounds__(THREADS, 1) bwd_main2_kernel(const __grid_cons
                 bulk_load(smem_u32(smem + SM::ROW_OFF + st * 512), rows + qt * (2 * BQ2), 512, qb);
             }
             __syncwarp();
-            if (mtma && i + MSK_STAGES - 1 < n_qt) load_mask(i + MSK_STAGES - 1);
+            if (mtma && !(i & 1) && i / 2 + MSK_STAGES - 1 < n_pairs_q) load_mask(i / 2 + MSK_STAGES - 1);
             mbar_wait(smem_u32(&do_empty[st]), ph ^ 1);
             if (elect_one()) {
                 const uint32_t db = smem_u32(&do_full[st]);
@@ -1070,9 +1074,9 @@ __global__ void __launch_bounds__(THREADS, 1) bwd_main2_kernel(const __grid_cons
             const float* Dv = nlse + BQ2;
 #if defined(RGO_BWD_DIAG) && (RGO_BWD_DIAG & 1)  // timing diagnostic: no softmax/dS work
             if (MODE == MASK_BITS && p.mask_tma) {
-                mbar_wait(smem_u32(&m_full[i % MSK_STAGES]), (i / MSK_STAGES) & 1);
+                mbar_wait(smem_u32(&m_full[(i / 2) % MSK_STAGES]), ((i / 2) / MSK_STAGES) & 1);
                 __syncwarp();
-                if (lane == 0) mbar_arrive(smem_u32(&m_empty[i % MSK_STAGES]));
+                if (lane == 0 && (i & 1)) mbar_arrive(smem_u32(&m_empty[(i / 2) % MSK_STAGES]));
             }
             mbar_wait(smem_u32(&q_full[st]), ph);
             mbar_wait(smem_u32(s_full), i & 1);
@@ -1087,11 +1091,12 @@ __global__ void __launch_bounds__(THREADS, 1) bwd_main2_kernel(const __grid_cons
 #endif
             uint32_t w = 0;
             if (MODE == MASK_BITS && p.mask_tma) {  // this lane's query row, this warp's 32 keys, from smem
-                const int ms = i % MSK_STAGES;
-                mbar_wait(smem_u32(&m_full[ms]), (i / MSK_STAGES) & 1);
-                w = reinterpret_cast<const uint32_t*>(smem + SM::MSK_OFF + ms * 1024)[(32 * h + lane) * 4 + qw];
+                const int ms = (i / 2) % MSK_STAGES;
+                mbar_wait(smem_u32(&m_full[ms]), ((i / 2) / MSK_STAGES) & 1);
+                w = reinterpret_cast<const uint32_t*>(smem + SM::MSK_OFF + ms * MSK_SLOT)
+                    [((i & 1) * BQ2 + 32 * h + lane) * 4 + qw];
                 __syncwarp();
-                if (lane == 0) mbar_arrive(smem_u32(&m_empty[ms]));  // slot free (the word is in a register)
+                if (lane == 0 && (i & 1)) mbar_arrive(smem_u32(&m_empty[ms]));  // both tiles' words read
                 mbar_wait(smem_u32(&q_full[st]), ph);  // row terms of tile i landed
             } else {
                 if (qrow < p.S)
@@ -1732,7 +1737,7 @@ static cudaError_t launch_attn_bwd2(const AttnBwdJob& j, cudaStream_t s) {
     if (mode == rgo_attn::MASK_BITS && j.S % 128 == 0 && (reinterpret_cast<uintptr_t>(j.bits) & 15) == 0) {
         const uint64_t dims[2] = {static_cast<uint64_t>(j.S) / 8, static_cast<uint64_t>(j.B) * j.H * j.S};
         const uint64_t strides[1] = {static_cast<uint64_t>(j.S) / 8};
-        const uint32_t box[2] = {16, static_cast<uint32_t>(BQ2)};
+        const uint32_t box[2] = {16, static_cast<uint32_t>(2 * BQ2)};
         p.mask_tma = make_tmap(&tm, j.bits, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, dims, strides, box,
                                CU_TENSOR_MAP_SWIZZLE_NONE) ? 1 : 0;
     }
