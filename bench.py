@@ -29,8 +29,15 @@ sys.path.insert(0, ROOT)
 L = dict(batch=4, seq=4096, heads=32, head_dim=128, ffn=11008, keep_prob=0.9, rounds=10)
 
 
+# The headline line once the main measurement is complete (extras are added to the same
+# dict as they finish) and the section running now: the watchdog prints the line it has
+# rather than losing the headline to a wedged extra.
+_PARTIAL = {"line": None, "section": None}
+
+
 def log(msg):
     """Progress on stderr (the JSON line is the only stdout output)."""
+    _PARTIAL["section"] = msg
     if int(os.environ.get("RANK", "0")) == 0:
         print(f"[bench {time.strftime('%H:%M:%S')}] {msg}", file=sys.stderr, flush=True)
 
@@ -955,6 +962,7 @@ def bench_block(args, rank, world):
         "energy": energy,
         "clocks": clocks, "gpu_launches": launches[best],
     }
+    _PARTIAL["line"] = line
     if not args.no_extras:
         # K2 stand-alone: the block's four FP8 GEMMs (their epilogues as in the block),
         # each timed alone on unit-variance e4m3 data, against the FP8 peak
@@ -1094,7 +1102,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true",
                     help="skip the secondary configs (GPT-3 block, attention fwd+bwd, SQ sweep)")
-    ap.add_argument("--watchdog-s", type=float, default=1200.0,
+    ap.add_argument("--watchdog-s", type=float, default=600.0,
                     help="exit with an error line if the GPU part has not finished after this many seconds (0 = off)")
     args = ap.parse_args()
 
@@ -1128,9 +1136,17 @@ def main():
     import threading
 
     def _watchdog():
-        log(f"watchdog: no result after {args.watchdog_s} s, exiting")
-        print(json.dumps({"metric": "llama2_block_ms", "error": f"watchdog: no result after {args.watchdog_s} s"}),
-              flush=True)
+        section = _PARTIAL["section"]
+        log(f"watchdog: no result after {args.watchdog_s} s (in: {section}), exiting")
+        if rank == 0 and _PARTIAL["line"] is not None:
+            # the headline was measured: report it with the extras that completed
+            out = dict(_PARTIAL["line"])
+            out["watchdog"] = f"extras incomplete: no progress after {args.watchdog_s} s in '{section}'"
+            print(json.dumps(out), flush=True)
+            os._exit(0)
+        if rank == 0:
+            print(json.dumps({"metric": "llama2_block_ms",
+                              "error": f"watchdog: no result after {args.watchdog_s} s (in: {section})"}), flush=True)
         os._exit(3)
 
     wd = threading.Timer(args.watchdog_s, _watchdog)
