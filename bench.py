@@ -32,12 +32,13 @@ L = dict(batch=4, seq=4096, heads=32, head_dim=128, ffn=11008, keep_prob=0.9, ro
 # The headline line once the main measurement is complete (extras are added to the same
 # dict as they finish) and the section running now: the watchdog prints the line it has
 # rather than losing the headline to a wedged extra.
-_PARTIAL = {"line": None, "section": None}
+_PARTIAL = {"line": None, "section": None, "since": time.time()}
 
 
 def log(msg):
     """Progress on stderr (the JSON line is the only stdout output)."""
     _PARTIAL["section"] = msg
+    _PARTIAL["since"] = time.time()
     if int(os.environ.get("RANK", "0")) == 0:
         print(f"[bench {time.strftime('%H:%M:%S')}] {msg}", file=sys.stderr, flush=True)
 
@@ -1102,6 +1103,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true",
                     help="skip the secondary configs (GPT-3 block, attention fwd+bwd, SQ sweep)")
+    ap.add_argument("--stall-s", type=float, default=240.0,
+                    help="watchdog: exit (printing what was measured) if one section makes no progress this long")
     ap.add_argument("--watchdog-s", type=float, default=600.0,
                     help="exit with an error line if the GPU part has not finished after this many seconds (0 = off)")
     args = ap.parse_args()
@@ -1137,20 +1140,31 @@ def main():
 
     def _watchdog():
         section = _PARTIAL["section"]
-        log(f"watchdog: no result after {args.watchdog_s} s (in: {section}), exiting")
+        log(f"watchdog: no progress (limit {args.watchdog_s} s, or {args.stall_s} s in one section) "
+            f"in: {section}; exiting")
         if rank == 0 and _PARTIAL["line"] is not None:
             # the headline was measured: report it with the extras that completed
             out = dict(_PARTIAL["line"])
-            out["watchdog"] = f"extras incomplete: no progress after {args.watchdog_s} s in '{section}'"
+            out["watchdog"] = f"extras incomplete: wedged in '{section}' (no progress for {args.stall_s} s)"
             print(json.dumps(out), flush=True)
             os._exit(0)
         if rank == 0:
             print(json.dumps({"metric": "llama2_block_ms",
-                              "error": f"watchdog: no result after {args.watchdog_s} s (in: {section})"}), flush=True)
+                              "error": f"watchdog: wedged in '{section}' (limits: {args.watchdog_s} s total, "
+                                       f"{args.stall_s} s per section)"}), flush=True)
         os._exit(3)
 
-    wd = threading.Timer(args.watchdog_s, _watchdog)
-    wd.daemon = True
+    wd_stop = threading.Event()
+    t_start = time.time()
+
+    def _watch():  # total limit, and a per-section stall limit (every section takes < 1 min)
+        while not wd_stop.wait(2.0):
+            now = time.time()
+            if now - t_start > args.watchdog_s or now - _PARTIAL["since"] > args.stall_s:
+                _watchdog()
+
+    wd = threading.Thread(target=_watch, daemon=True)
+    _PARTIAL["since"] = time.time()
     if args.watchdog_s > 0:
         wd.start()
     line = bench_block(args, rank, world) if args.workload == "block" else bench_mask_only(args, rank, world)
@@ -1158,7 +1172,7 @@ def main():
         import paper_2410_07531_b200 as rgo
         log("drop-in e2e at config O (host arrays through the C ABI)")
         line["e2e_dropin_O"] = bench_dropin_O(rgo)
-    wd.cancel()
+    wd_stop.set()
     if rank == 0:
         if not args.no_cpu_baseline and world == 1:  # the CPU baseline is an N=1 measurement
             log("CPU baseline (reference, host cores)")
